@@ -1,0 +1,132 @@
+/*
+ * icq_b200.h — C ABI of the B200-native ICQ query path (libicq_b200.so).
+ *
+ * Drop-in boundary for the reference package's query engines
+ * (/root/reference/pkg/src/icq/search.py).  The reference is pure Python,
+ * so its "FFI" is the Python call surface; each entry point below names the
+ * reference function it replaces (file:line) and keeps its argument meaning
+ * and error behaviour.  The ctypes binding a maintainer adds on the reference
+ * side is shown in INTEGRATION.md; the package paper_1912_08756_b200 ships it.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "dev" pointers are CUDA device
+ *     pointers; "host" pointers are ordinary host memory.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every function returns an icq_status; on failure a thread-local message
+ *     is available from icq_last_error().  Nothing throws across the ABI.
+ *   - Results are exactly the reference's: ids/int64, scores/float64 (the
+ *     reference's float64 distance values, search.py:163), refinement counts.
+ *     The fp32 hot path is certified against float64 with a rounding-error
+ *     bound, so survivor sets and top-k match the float64 reference bit for bit.
+ */
+#ifndef ICQ_B200_H
+#define ICQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ICQ_OK = 0,
+  ICQ_ERR_VALIDATION = 1,   /* -> icq.data.ValidationError (data.py:32) */
+  ICQ_ERR_UNSUPPORTED = 2,  /* shape outside this build (m > 256, K > 16, k too large) */
+  ICQ_ERR_CUDA = 3,         /* CUDA runtime / launch failure */
+  ICQ_ERR_NOMEM = 4         /* device allocation failed / workspace too small */
+} icq_status;
+
+typedef struct icq_index_s* icq_index_t;
+
+/* Message of the last failing call on this host thread ("" if none). */
+const char* icq_last_error(void);
+
+/* ABI version (bumped on any signature change). */
+int32_t icq_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Index: device-resident copy of icq.data.SearchIndex (data.py:193-263).
+ *   books : host float32 [K*m*d], row-major (K, m, d)        (data.py:143, :222)
+ *   codes : host uint32  [n*K],   row-major (n, K)           (data.py:179)
+ *   fast  : host uint32  [F], sorted unique book ids < K     (data.py:159-164)
+ * Validation mirrors SearchIndex.__post_init__: code >= m, unsorted/duplicate
+ * fast set or fast id >= K -> ICQ_ERR_VALIDATION.  m > 256 or K > 16 ->
+ * ICQ_ERR_UNSUPPORTED (codes are repacked to uint8 on the device).
+ * The handle is immutable after creation and may be shared by threads.
+ * ------------------------------------------------------------------------- */
+icq_status icq_index_create(const float* books_host, int32_t K, int32_t m, int32_t d,
+                            const uint32_t* codes_host, int64_t n,
+                            const uint32_t* fast_host, int32_t F,
+                            icq_index_t* out);
+
+/* Same, with codes already narrowed to uint8 (host). */
+icq_status icq_index_create_u8(const float* books_host, int32_t K, int32_t m, int32_t d,
+                               const uint8_t* codes_host, int64_t n,
+                               const uint32_t* fast_host, int32_t F,
+                               icq_index_t* out);
+
+/* Same, all inputs already on the device (codes uint8 (n, K) row-major). */
+icq_status icq_index_create_device(const float* books_dev, int32_t K, int32_t m, int32_t d,
+                                   const uint8_t* codes_dev, int64_t n,
+                                   const uint32_t* fast_host, int32_t F,
+                                   void* stream, icq_index_t* out);
+
+icq_status icq_index_destroy(icq_index_t h);
+
+/* Shape and device footprint of an index. */
+icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int32_t* d,
+                          int32_t* F, int64_t* device_bytes);
+
+/* ---------------------------------------------------------------------------
+ * build_lut (search.py:61-69): lut[q][b][j] = sum_d (c[b][j][d] - q[d])^2 in
+ * float64, summed in numpy's pairwise order (bitwise equal to the reference).
+ *   q   : dev float64 [Q*d]      lut : dev float64 [Q*K*m]
+ * ------------------------------------------------------------------------- */
+icq_status icq_build_lut(icq_index_t h, const double* q_dev, int32_t Q, double* lut_dev,
+                         void* stream);
+
+/* Device workspace needed by the search calls below for Q queries, top-k. */
+icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes);
+
+/* ---------------------------------------------------------------------------
+ * search_two_step (search.py:112-165), batched: Q independent queries.
+ *   sigma        : pruning margin >= 0 (NaN or negative -> ICQ_ERR_VALIDATION,
+ *                  search.py:125-126); pass the index margin for sigma=None.
+ *   k            : 1 <= k <= n (search.py:56-58)
+ *   ids_dev      : int64 [Q*k]   ascending (score, id), search.py:156
+ *   scores_dev   : float64 [Q*k]
+ *   refine_dev   : int64 [Q]     ops.refinements (search.py:160); may be NULL
+ *   survivors_dev: optional uint32 bitmap [Q * ceil(n/32)] of refined ids
+ *                  (instrumentation for parity tests; NULL to skip)
+ *   stats_dev    : optional int64 [Q*4] diagnostics per query: heap insertions,
+ *                  items examined by the in-order replay, items certified in
+ *                  float64 (near-ties of the fp32 filter), replayed groups
+ *   fallback_out : optional host int32; set to 1 when the fast set is empty and
+ *                  the exact engine ran instead (search.py:127-131)
+ * The call is asynchronous on `stream` (no host synchronisation).
+ * ------------------------------------------------------------------------- */
+icq_status icq_search_two_step(icq_index_t h, const double* q_dev, int32_t Q, int32_t k,
+                               double sigma, int64_t* ids_dev, double* scores_dev,
+                               int64_t* refine_dev, uint32_t* survivors_dev,
+                               int64_t* stats_dev, int32_t* fallback_out,
+                               void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* search_exact (search.py:97-109): full scan, top-k by (score, id). */
+icq_status icq_search_exact(icq_index_t h, const double* q_dev, int32_t Q, int32_t k,
+                            int64_t* ids_dev, double* scores_dev,
+                            void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer entry points (end-to-end: H2D of queries, search, D2H of results,
+ * synchronous).  Same semantics as above; all pointers are host pointers.
+ * `exact` = 0 -> two-step, 1 -> exact engine.
+ * ------------------------------------------------------------------------- */
+icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32_t k,
+                           double sigma, int32_t exact, int64_t* ids_host,
+                           double* scores_host, int64_t* refine_host, int32_t* fallback_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ICQ_B200_H */

@@ -1,0 +1,378 @@
+// icq_capi.cu — extern "C" boundary (include/icq_b200.h) and index repack.
+//
+// Replaces the Python entry points of /root/reference/pkg/src/icq/search.py
+// (build_lut :61, search_exact :97, search_two_step :112) and the argument
+// layout of icq.data.SearchIndex (data.py:193-263).  Validation mirrors
+// search.py:47-58, :123-131 and data.py:145-176.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/icq_b200.h"
+#include "icq_types.cuh"
+
+
+using namespace icq;
+
+static thread_local std::string g_err;
+
+static icq_status fail(icq_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(ICQ_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                             \
+  } while (0)
+
+struct icq_index_s {
+  int32_t K, m, d, F, KP, FP;
+  int64_t n, n_pad;
+  float* books;
+  uint8_t* codes_full;
+  uint8_t* codes_fast;
+  bool fast_alias;
+  uint8_t fast_books[kMaxK];
+  LutProg* prog_dev;
+  int32_t* err_dev;
+  int64_t bytes;
+};
+
+static int pow2_ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+// --------------------------------------------------------------------------
+// repack: (n, K) codes -> uint8 full rows (stride KP) + fast rows (stride FP)
+// --------------------------------------------------------------------------
+template <typename CodeT>
+__global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t n, int K, int m, int KP,
+                              uint8_t* __restrict__ full, int FP, int F, const FastBooks fb,
+                              uint8_t* __restrict__ fastp, int32_t* err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint8_t row[kMaxK];
+  bool bad = false;
+  for (int b = 0; b < K; ++b) {
+    const uint64_t c = (uint64_t)codes[i * K + b];
+    bad |= c >= (uint64_t)m;
+    row[b] = (uint8_t)c;
+  }
+  if (bad) atomicOr(err, 2);
+  for (int b = 0; b < KP; ++b) full[i * KP + b] = b < K ? row[b] : 0;
+  if (fastp) {
+    for (int s = 0; s < FP; ++s) fastp[i * FP + s] = s < F ? row[fb.b[s]] : 0;
+  }
+}
+
+template <typename CodeT>
+static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t d,
+                              const CodeT* codes, int64_t n, const uint32_t* fast, int32_t F,
+                              bool on_device, cudaStream_t stream, icq_index_t* out) {
+  if (!out) return fail(ICQ_ERR_VALIDATION, "out handle pointer is NULL");
+  *out = nullptr;
+  if (K < 1) return fail(ICQ_ERR_VALIDATION, "K must be >= 1, got %d", K);
+  if (m < 2) return fail(ICQ_ERR_VALIDATION, "m must be >= 2, got %d", m);
+  if (d < 1) return fail(ICQ_ERR_VALIDATION, "d must be >= 1, got %d", d);
+  if (n < 1) return fail(ICQ_ERR_VALIDATION, "index must hold at least one element");
+  if (K > kMaxK) return fail(ICQ_ERR_UNSUPPORTED, "K=%d > %d books is not supported", K, kMaxK);
+  if (m > 256) return fail(ICQ_ERR_UNSUPPORTED, "m=%d > 256 codewords (uint8 codes)", m);
+  if (n > 0x7fffffffLL) return fail(ICQ_ERR_UNSUPPORTED, "n=%lld exceeds int32 ids", (long long)n);
+  if (F < 0 || F > K) return fail(ICQ_ERR_VALIDATION, "fast set must hold codebook indices in [0, K)");
+  for (int s = 0; s < F; ++s) {
+    if (fast[s] >= (uint32_t)K)
+      return fail(ICQ_ERR_VALIDATION, "fast set must hold codebook indices in [0, K)");
+    if (s && fast[s] <= fast[s - 1])
+      return fail(ICQ_ERR_VALIDATION, "fast set must be sorted and unique");
+  }
+  LutProg prog;
+  if (!make_lut_prog(d, &prog)) return fail(ICQ_ERR_UNSUPPORTED, "d=%d out of range [1, 8192]", d);
+
+  auto* h = new icq_index_s();
+  h->K = K; h->m = m; h->d = d; h->F = F; h->n = n;
+  h->KP = pow2_ceil(K);
+  h->FP = F ? pow2_ceil(F) : 0;
+  h->n_pad = (n + 8191) / 8192 * 8192;
+  memset(h->fast_books, 0, sizeof(h->fast_books));
+  bool prefix = true;
+  for (int s = 0; s < F; ++s) {
+    h->fast_books[s] = (uint8_t)fast[s];
+    prefix &= fast[s] == (uint32_t)s;
+  }
+  h->fast_alias = F > 0 && prefix && h->FP == h->KP;
+
+  auto cleanup = [&](icq_status st) {
+    cudaFree(h->books); cudaFree(h->codes_full);
+    if (!h->fast_alias) cudaFree(h->codes_fast);
+    cudaFree(h->prog_dev); cudaFree(h->err_dev);
+    delete h;
+    return st;
+  };
+  const size_t bbytes = (size_t)K * m * d * sizeof(float);
+  const size_t fullb = (size_t)h->n_pad * h->KP;
+  const size_t fastb = (F && !h->fast_alias) ? (size_t)h->n_pad * h->FP : 0;
+  cudaError_t e;
+  if ((e = cudaMalloc(&h->books, bbytes)) != cudaSuccess ||
+      (e = cudaMalloc(&h->codes_full, fullb)) != cudaSuccess ||
+      (fastb && (e = cudaMalloc(&h->codes_fast, fastb)) != cudaSuccess) ||
+      (e = cudaMalloc(&h->prog_dev, sizeof(LutProg))) != cudaSuccess ||
+      (e = cudaMalloc(&h->err_dev, sizeof(int32_t))) != cudaSuccess) {
+    fail(ICQ_ERR_NOMEM, "device allocation failed: %s", cudaGetErrorString(e));
+    return cleanup(ICQ_ERR_NOMEM);
+  }
+  if (h->fast_alias) h->codes_fast = h->codes_full;
+  h->bytes = (int64_t)(bbytes + fullb + fastb);
+
+  const CodeT* codes_dev = codes;
+  CodeT* staged = nullptr;
+  auto run = [&]() -> cudaError_t {
+    cudaError_t e2;
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if ((e2 = cudaMemcpyAsync(h->books, books, bbytes, kind, stream)) != cudaSuccess) return e2;
+    if ((e2 = cudaMemcpyAsync(h->prog_dev, &prog, sizeof(LutProg), cudaMemcpyHostToDevice,
+                              stream)) != cudaSuccess) return e2;
+    if ((e2 = cudaMemsetAsync(h->err_dev, 0, sizeof(int32_t), stream)) != cudaSuccess) return e2;
+    if ((e2 = cudaMemsetAsync(h->codes_full, 0, fullb, stream)) != cudaSuccess) return e2;
+    if (fastb && (e2 = cudaMemsetAsync(h->codes_fast, 0, fastb, stream)) != cudaSuccess) return e2;
+    if (!on_device) {
+      const size_t cb = (size_t)n * K * sizeof(CodeT);
+      if ((e2 = cudaMalloc(&staged, cb)) != cudaSuccess) return e2;
+      if ((e2 = cudaMemcpyAsync(staged, codes, cb, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
+        return e2;
+      codes_dev = staged;
+    }
+    FastBooks fb;
+    memset(&fb, 0, sizeof(fb));
+    for (int s = 0; s < F; ++s) fb.b[s] = (uint8_t)fast[s];
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+    repack_kernel<CodeT><<<blocks, threads, 0, stream>>>(
+        codes_dev, n, K, m, h->KP, h->codes_full, h->FP, F, fb,
+        (F && !h->fast_alias) ? h->codes_fast : nullptr, h->err_dev);
+    if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
+    return cudaStreamSynchronize(stream);
+  };
+  e = run();
+  if (staged) cudaFree(staged);
+  if (e != cudaSuccess) {
+    fail(ICQ_ERR_CUDA, "index upload/repack failed: %s", cudaGetErrorString(e));
+    return cleanup(ICQ_ERR_CUDA);
+  }
+  int32_t err = 0;
+  cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost);
+  if (err & 2) {
+    fail(ICQ_ERR_VALIDATION, "codes reference codewords beyond m");
+    return cleanup(ICQ_ERR_VALIDATION);
+  }
+  *out = h;
+  g_err.clear();
+  return ICQ_OK;
+}
+
+extern "C" {
+
+const char* icq_last_error(void) { return g_err.c_str(); }
+
+int32_t icq_abi_version(void) { return 1; }
+
+icq_status icq_index_create(const float* books, int32_t K, int32_t m, int32_t d,
+                            const uint32_t* codes, int64_t n, const uint32_t* fast, int32_t F,
+                            icq_index_t* out) {
+  return create_impl<uint32_t>(books, K, m, d, codes, n, fast, F, false, 0, out);
+}
+
+icq_status icq_index_create_u8(const float* books, int32_t K, int32_t m, int32_t d,
+                               const uint8_t* codes, int64_t n, const uint32_t* fast, int32_t F,
+                               icq_index_t* out) {
+  return create_impl<uint8_t>(books, K, m, d, codes, n, fast, F, false, 0, out);
+}
+
+icq_status icq_index_create_device(const float* books, int32_t K, int32_t m, int32_t d,
+                                   const uint8_t* codes, int64_t n, const uint32_t* fast,
+                                   int32_t F, void* stream, icq_index_t* out) {
+  return create_impl<uint8_t>(books, K, m, d, codes, n, fast, F, true, (cudaStream_t)stream, out);
+}
+
+icq_status icq_index_destroy(icq_index_t h) {
+  if (!h) return ICQ_OK;
+  cudaFree(h->books);
+  cudaFree(h->codes_full);
+  if (!h->fast_alias) cudaFree(h->codes_fast);
+  cudaFree(h->prog_dev);
+  cudaFree(h->err_dev);
+  delete h;
+  return ICQ_OK;
+}
+
+icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int32_t* d,
+                          int32_t* F, int64_t* device_bytes) {
+  if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  if (n) *n = h->n;
+  if (K) *K = h->K;
+  if (m) *m = h->m;
+  if (d) *d = h->d;
+  if (F) *F = h->F;
+  if (device_bytes) *device_bytes = h->bytes;
+  return ICQ_OK;
+}
+
+icq_status icq_build_lut(icq_index_t h, const double* q, int32_t Q, double* lut, void* stream) {
+  if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
+  if (Q == 0) return ICQ_OK;
+  CUDA_TRY(launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, (cudaStream_t)stream));
+  return ICQ_OK;
+}
+
+icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes) {
+  if (!h || !bytes) return fail(ICQ_ERR_VALIDATION, "null argument");
+  (void)k;
+  *bytes = (size_t)(Q > 0 ? Q : 0) * h->K * h->m * sizeof(double) + 256;
+  return ICQ_OK;
+}
+
+static icq_status search_impl(icq_index_t h, const double* q, int32_t Q, int32_t k, double sigma,
+                              bool exact, int64_t* ids, double* scores, int64_t* refine,
+                              uint32_t* survivors, int64_t* stats, int32_t* fallback_out,
+                              void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  if (!(k >= 1 && (int64_t)k <= h->n))
+    return fail(ICQ_ERR_VALIDATION, "k=%d out of range [1, %lld]", k, (long long)h->n);
+  if (!exact && !(sigma >= 0)) return fail(ICQ_ERR_VALIDATION, "sigma must be >= 0, got %g", sigma);
+  if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
+  const bool fallback = !exact && h->F == 0;  // search.py:127-131
+  if (fallback_out) *fallback_out = fallback ? 1 : 0;
+  if (fallback) exact = true;
+  if (Q == 0) return ICQ_OK;
+  size_t need = 0;
+  icq_workspace_size(h, Q, k, &need);
+  if (!ws || ws_bytes < need)
+    return fail(ICQ_ERR_NOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  double* lut = reinterpret_cast<double*>(ws);
+  CUDA_TRY(launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, s));
+  if (survivors) {
+    const int64_t words = (h->n + 31) / 32;
+    CUDA_TRY(cudaMemsetAsync(survivors, 0, (size_t)Q * words * sizeof(uint32_t), s));
+  }
+  ScanParams p;
+  memset(&p, 0, sizeof(p));
+  p.codes_full = h->codes_full;
+  p.lut64 = lut;
+  p.ids = ids;
+  p.scores = scores;
+  p.refinements = exact ? nullptr : refine;
+  p.survivors = exact ? nullptr : survivors;
+  p.stats = stats;
+  p.error = h->err_dev;
+  p.n = h->n;
+  p.words = (h->n + 31) / 32;
+  p.K = h->K;
+  p.m = h->m;
+  p.KP = h->KP;
+  p.k = k;
+  int FP;
+  if (exact) {
+    p.codes_fast = h->codes_full;
+    p.F = h->K;
+    FP = h->KP;
+    for (int b = 0; b < h->K; ++b) p.fast_books[b] = (uint8_t)b;
+    p.sigma = 0.0;
+  } else {
+    p.codes_fast = h->codes_fast;
+    p.F = h->F;
+    FP = h->FP;
+    memcpy(p.fast_books, h->fast_books, sizeof(p.fast_books));
+    p.sigma = sigma;
+  }
+  int unsupported = 0;
+  CUDA_TRY(launch_scan(p, FP, Q, s, &unsupported));
+  if (unsupported)
+    return fail(ICQ_ERR_UNSUPPORTED, "k=%d does not fit the on-chip heap for K=%d, m=%d", k, h->K,
+                h->m);
+  if (exact && refine) {
+    // search_exact reports refinements = n (search.py:108)
+    std::vector<int64_t> nn((size_t)Q, h->n);
+    CUDA_TRY(cudaMemcpyAsync(refine, nn.data(), (size_t)Q * sizeof(int64_t),
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  return ICQ_OK;
+}
+
+icq_status icq_search_two_step(icq_index_t h, const double* q, int32_t Q, int32_t k, double sigma,
+                               int64_t* ids, double* scores, int64_t* refine, uint32_t* survivors,
+                               int64_t* stats, int32_t* fallback_out, void* ws, size_t ws_bytes,
+                               void* stream) {
+  return search_impl(h, q, Q, k, sigma, false, ids, scores, refine, survivors, stats,
+                     fallback_out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+icq_status icq_search_exact(icq_index_t h, const double* q, int32_t Q, int32_t k, int64_t* ids,
+                            double* scores, void* ws, size_t ws_bytes, void* stream) {
+  return search_impl(h, q, Q, k, 0.0, true, ids, scores, nullptr, nullptr, nullptr, nullptr, ws,
+                     ws_bytes, (cudaStream_t)stream);
+}
+
+icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32_t k,
+                           double sigma, int32_t exact, int64_t* ids_host, double* scores_host,
+                           int64_t* refine_host, int32_t* fallback_out) {
+  if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
+  if (!(k >= 1 && (int64_t)k <= h->n))
+    return fail(ICQ_ERR_VALIDATION, "k=%d out of range [1, %lld]", k, (long long)h->n);
+  if (!exact && !(sigma >= 0)) return fail(ICQ_ERR_VALIDATION, "sigma must be >= 0, got %g", sigma);
+  if (fallback_out) *fallback_out = (!exact && h->F == 0) ? 1 : 0;
+  if (Q == 0) return ICQ_OK;
+  cudaStream_t s = cudaStreamPerThread;
+  size_t ws_bytes = 0;
+  icq_workspace_size(h, Q, k, &ws_bytes);
+  const size_t qb = (size_t)Q * h->d * sizeof(double);
+  const size_t ib = (size_t)Q * k * sizeof(int64_t);
+  const size_t sb = (size_t)Q * k * sizeof(double);
+  const size_t rb = (size_t)Q * sizeof(int64_t);
+  char* buf = nullptr;
+  const size_t total = ws_bytes + qb + ib + sb + rb + 4 * 256;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, total, s));
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  char* ws = buf;
+  double* qd = reinterpret_cast<double*>(buf + al(ws_bytes));
+  int64_t* idd = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(qd) + al(qb));
+  double* scd = reinterpret_cast<double*>(reinterpret_cast<char*>(idd) + al(ib));
+  int64_t* rfd = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scd) + al(sb));
+  icq_status st = ICQ_OK;
+  cudaError_t e = cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    st = search_impl(h, qd, Q, k, sigma, exact != 0, idd, scd, rfd, nullptr, nullptr, nullptr, ws,
+                     ws_bytes, s);
+    if (st == ICQ_OK) {
+      e = cudaMemcpyAsync(ids_host, idd, ib, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, sb, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess && refine_host)
+        e = cudaMemcpyAsync(refine_host, rfd, rb, cudaMemcpyDeviceToHost, s);
+    }
+  }
+  cudaFreeAsync(buf, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (st != ICQ_OK) return st;
+  if (e != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e2));
+  int32_t err = 0;
+  CUDA_TRY(cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err & 1) return fail(ICQ_ERR_CUDA, "scan kernel shared-memory layout check failed");
+  return ICQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+"""Argument containers of the query path (mirror of icq.data, data.py:32-263).
+
+The B200 engines accept either these containers or the reference's own
+``icq.SearchIndex`` objects (duck-typed: ``books.codewords``, ``codes.codes``,
+``fast``, ``sigma``, ``cfg.K``/``cfg.m``).  Validation restates
+``SearchIndex.__post_init__`` (data.py:136-176) so the same inputs are
+rejected with the same exception class.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+class ValidationError(ValueError):
+    """Invalid values: non-finite data, bad shapes, out-of-range parameters (data.py:32)."""
+
+
+class UnsupportedError(RuntimeError):
+    """Inputs valid for the reference but outside this build's kernels (m > 256, K > 16)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure inside the native library."""
+
+
+@dataclass
+class Config:
+    """Quantizer hyperparameters carried by an index (data.py:80-121; only K, m used here)."""
+
+    K: int = 8
+    m: int = 256
+    gamma1: float = 0.1
+    gamma2: float = 1.0
+    pi1: float = 0.9
+    pi2: float = 0.1
+    alpha2: float = -10.0
+    sigma_scale: float = 1.0
+    epochs: int = 50
+    batch_size: int = 256
+    learning_rate: float = 1e-2
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.K < 1:
+            raise ValidationError(f"K must be >= 1, got {self.K}")
+        if self.m < 2:
+            raise ValidationError(f"m must be >= 2, got {self.m}")
+
+
+@dataclass
+class CodebookSet:
+    """K codebooks of m codewords, (K, m, d) (data.py:136-164)."""
+
+    codewords: np.ndarray
+
+    def __post_init__(self):
+        cw = np.ascontiguousarray(self.codewords)
+        if cw.ndim != 3:
+            raise ValidationError(f"codewords must be (K, m, d), got shape {cw.shape}")
+        self.codewords = cw
+
+    @property
+    def K(self) -> int:
+        return self.codewords.shape[0]
+
+    @property
+    def m(self) -> int:
+        return self.codewords.shape[1]
+
+    @property
+    def d(self) -> int:
+        return self.codewords.shape[2]
+
+
+@dataclass
+class CodeMatrix:
+    """(n, K) codeword choices (data.py:167-190); stored uint32 like the reference."""
+
+    codes: np.ndarray
+
+    def __post_init__(self):
+        c = np.ascontiguousarray(self.codes)
+        if c.ndim != 2:
+            raise ValidationError(f"codes must be (n, K), got shape {c.shape}")
+        if c.size and np.any(c < 0):
+            raise ValidationError("codes must be non-negative")
+        self.codes = c.astype(np.uint32, copy=False)
+
+    @property
+    def n(self) -> int:
+        return self.codes.shape[0]
+
+    @property
+    def K(self) -> int:
+        return self.codes.shape[1]
+
+
+@dataclass
+class SearchIndex:
+    """Query-time state of a trained quantizer (data.py:193-263)."""
+
+    books: CodebookSet
+    codes: CodeMatrix
+    xi: np.ndarray
+    fast: np.ndarray
+    sigma: float
+    lambdas: np.ndarray
+    cfg: Config = field(default_factory=Config)
+
+    def __post_init__(self):
+        books = self.books if isinstance(self.books, CodebookSet) else CodebookSet(self.books)
+        codes = self.codes if isinstance(self.codes, CodeMatrix) else CodeMatrix(self.codes)
+        self.books = CodebookSet(books.codewords.astype(np.float32, copy=False))
+        self.codes = codes
+        if codes.K != books.K:
+            raise ValidationError(f"codes have {codes.K} books, codebooks have {books.K}")
+        if codes.codes.size and codes.codes.max() >= books.m:
+            raise ValidationError("codes reference codewords beyond m")
+        if self.cfg.K != books.K or self.cfg.m != books.m:
+            raise ValidationError("config K/m disagree with the codebooks")
+        xi = np.ascontiguousarray(np.asarray(self.xi), dtype=np.uint8)
+        if xi.shape != (books.d,):
+            raise ValidationError(f"xi length {xi.shape} does not match d={books.d}")
+        if xi.size and xi.max() > 1:
+            raise ValidationError("xi entries must be 0 or 1")
+        self.xi = xi
+        fast = np.ascontiguousarray(np.asarray(self.fast), dtype=np.uint32)
+        if fast.ndim != 1 or (fast.size and fast.max() >= books.K):
+            raise ValidationError("fast set must hold codebook indices in [0, K)")
+        if fast.size and np.any(np.diff(fast.astype(np.int64)) <= 0):
+            raise ValidationError("fast set must be sorted and unique")
+        self.fast = fast
+        lam = np.ascontiguousarray(np.asarray(self.lambdas), dtype=np.float32)
+        if lam.shape != (books.d,):
+            raise ValidationError(f"lambdas length {lam.shape} does not match d={books.d}")
+        if lam.size and (not np.all(np.isfinite(lam)) or lam.min() < 0):
+            raise ValidationError("lambdas must be finite and non-negative")
+        self.lambdas = lam
+        sigma = float(np.float32(self.sigma))
+        if not np.isfinite(sigma) or sigma < 0:
+            raise ValidationError(f"sigma must be finite and >= 0, got {self.sigma}")
+        self.sigma = sigma
+
+    @property
+    def n(self) -> int:
+        return self.codes.n
+
+    @property
+    def d(self) -> int:
+        return self.books.d

@@ -145,6 +145,16 @@ def main():
     q = gmm(rng, 4, means, 0.3)
     save_case("trained_k16f4", idx, q, [10, 100], [0.0, 2.0])
 
+    # n == 1: numpy's gathered (1, K) array is C-contiguous, so the row sums
+    # run numpy's pairwise kernel instead of the column-sequential order
+    for K, F in ((9, 8), (16, 12)):
+        books = (rng.standard_normal((K, 5, 3)) * 7).astype(np.float32)
+        idx = SearchIndex(books=CodebookSet(books),
+                          codes=CodeMatrix(rng.integers(0, 5, size=(1, K))),
+                          xi=np.ones(3, dtype=np.uint8), fast=np.arange(F, dtype=np.uint32),
+                          sigma=0.0, lambdas=np.ones(3, dtype=np.float32), cfg=Config(K=K, m=5))
+        save_case(f"single_k{K}", idx, rng.normal(size=(3, 3)) * 5, [1], [0.0, 1e18])
+
 
 if __name__ == "__main__":
     sys.exit(main())

@@ -1,0 +1,174 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference golden vectors
+and vs the oracle.  Everything is bitwise: ids, float64 scores, refinement
+counts, op counters, and the survivor (refined-id) sets the reference only
+counts (search.py:150)."""
+
+import numpy as np
+import pytest
+
+from _golden import CASES, load
+from oracle import icq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1912_08756_b200 as icqb  # noqa: E402
+
+
+def _surv_ids(bitmap_row, n):
+    words = bitmap_row.astype(np.uint32)
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:n]
+    return np.flatnonzero(bits)
+
+
+def _index(c):
+    return icqb.SearchIndex(books=c.books, codes=c.codes, xi=np.ones(c.d, dtype=np.uint8),
+                            fast=c.fast, sigma=c.sigma,
+                            lambdas=np.ones(c.d, dtype=np.float32),
+                            cfg=icqb.Config(K=c.K, m=c.m))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_reference_api(name):
+    """Reference-shaped API (one query per call) == real reference outputs."""
+    c = load(name)
+    idx = _index(c)
+    for qi in range(len(c.luts)):
+        assert np.array_equal(icqb.build_lut(idx, c.queries[qi]), c.luts[qi])
+    for r in c.rows:
+        q = c.queries[r.query]
+        if r.is_exact:
+            got = icqb.search_exact(idx, q, r.k)
+        else:
+            got = icqb.search_two_step(idx, q, r.k, sigma=r.sigma)
+        assert np.array_equal(got.ids, r.ids), (name, r.query, r.k, r.sigma, r.is_exact)
+        assert np.array_equal(got.scores, r.scores), (name, r.query, r.k, r.sigma)
+        assert got.ops.fast_adds == r.fast_adds
+        assert got.ops.exact_adds == r.exact_adds
+        assert got.ops.lut_ops == r.lut_ops
+        assert got.ops.evaluations == r.evaluations
+        assert got.ops.refinements == r.refinements
+        assert got.fallback == r.fallback
+
+
+def _random_case(rng, n, d, K, m, F, dup=False, scale_fast=4.0):
+    books = rng.standard_normal((K, m, d)).astype(np.float32)
+    books[:F] *= scale_fast
+    codes = rng.integers(0, m, size=(n, K)).astype(np.uint8)
+    if dup:
+        codes[1::2] = codes[0::2]
+    fast = np.arange(F, dtype=np.uint32)
+    return books, codes, fast
+
+
+CONFIGS = [
+    # n,     d,  K,  m,  F, dup
+    (5000, 16, 8, 256, 2, False),
+    (5000, 16, 8, 256, 2, True),
+    (9000, 12, 16, 256, 4, False),
+    (3000, 8, 4, 16, 1, False),
+    (2500, 8, 5, 7, 3, True),
+    (7000, 20, 8, 256, 8, False),
+    (4100, 6, 16, 64, 16, False),
+    (20000, 32, 8, 256, 2, False),
+]
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+def test_random_vs_oracle_with_survivors(cfg):
+    n, d, K, m, F, dup = cfg
+    rng = np.random.default_rng(n + d + K + m + F)
+    books, codes, fast = _random_case(rng, n, d, K, m, F, dup)
+    dev = icqb.DeviceIndex(books, codes, fast)
+    Q = rng.standard_normal((6, d))
+    qd = torch.from_numpy(Q).cuda()
+    for k in (1, 10, 100):
+        for sigma in (0.0, 1.0, 25.0, 1e18):
+            out = dev.search_device(qd, k, sigma, survivors=True, stats=True)
+            torch.cuda.synchronize()
+            ids = out["ids"].cpu().numpy()
+            scores = out["scores"].cpu().numpy()
+            refine = out["refinements"].cpu().numpy()
+            surv = out["survivors"].cpu().numpy()
+            for i in range(Q.shape[0]):
+                ref = O.two_step(books, codes, fast, sigma, Q[i], k)
+                assert np.array_equal(ids[i], ref.ids), (cfg, k, sigma, i)
+                assert np.array_equal(scores[i], ref.scores), (cfg, k, sigma, i)
+                assert int(refine[i]) == ref.ops.refinements, (cfg, k, sigma, i)
+                assert np.array_equal(_surv_ids(surv[i], n), ref.survivors), (cfg, k, sigma, i)
+        out = dev.search_device(qd, k, exact=True)
+        torch.cuda.synchronize()
+        for i in range(Q.shape[0]):
+            ref = O.exact(books, codes, Q[i], k)
+            assert np.array_equal(out["ids"][i].cpu().numpy(), ref.ids)
+            assert np.array_equal(out["scores"][i].cpu().numpy(), ref.scores)
+
+
+def test_batch_invariance():
+    rng = np.random.default_rng(3)
+    books, codes, fast = _random_case(rng, 12000, 16, 8, 256, 2)
+    dev = icqb.DeviceIndex(books, codes, fast)
+    Q = rng.standard_normal((37, 16))
+    ids_all, sc_all, rf_all, _ = dev.search_host(Q, 25, 0.5, exact=False)
+    for i in (0, 5, 36):
+        ids1, sc1, rf1, _ = dev.search_host(Q[i:i + 1], 25, 0.5, exact=False)
+        assert np.array_equal(ids1[0], ids_all[i])
+        assert np.array_equal(sc1[0], sc_all[i])
+        assert rf1[0] == rf_all[i]
+
+
+def test_k_equals_n_and_tiny_n():
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 40):
+        books, codes, fast = _random_case(rng, n, 4, 3, 4, 2)
+        dev = icqb.DeviceIndex(books, codes, fast)
+        q = rng.standard_normal((2, 4))
+        for k in sorted({1, n}):
+            ids, scores, refine, _ = dev.search_host(q, k, 0.0, exact=False)
+            for i in range(2):
+                ref = O.two_step(books, codes, fast, 0.0, q[i], k)
+                assert np.array_equal(ids[i], ref.ids)
+                assert np.array_equal(scores[i], ref.scores)
+
+
+def test_validation_errors():
+    rng = np.random.default_rng(9)
+    books, codes, fast = _random_case(rng, 100, 4, 3, 4, 1)
+    dev = icqb.DeviceIndex(books, codes, fast)
+    q = rng.standard_normal((1, 4))
+    with pytest.raises(icqb.ValidationError):
+        dev.search_host(q, 0, 0.0, exact=False)
+    with pytest.raises(icqb.ValidationError):
+        dev.search_host(q, 101, 0.0, exact=False)
+    with pytest.raises(icqb.ValidationError):
+        dev.search_host(q, 3, -1.0, exact=False)
+    with pytest.raises(icqb.ValidationError):
+        dev.search_host(q, 3, float("nan"), exact=False)
+    bad = codes.copy()
+    bad[7, 1] = 4
+    with pytest.raises(icqb.ValidationError):
+        icqb.DeviceIndex(books, bad, fast)
+    with pytest.raises(icqb.ValidationError):
+        icqb.DeviceIndex(books, codes, np.array([1, 0], dtype=np.uint32))
+    with pytest.raises(icqb.UnsupportedError):
+        icqb.DeviceIndex(rng.standard_normal((2, 300, 4)).astype(np.float32),
+                         rng.integers(0, 300, size=(10, 2)).astype(np.uint32),
+                         np.array([0], dtype=np.uint32))
+
+
+def test_wide_mode_huge_values():
+    """LUT entries beyond float32 headroom: float64-only path, still exact."""
+    rng = np.random.default_rng(11)
+    books, codes, fast = _random_case(rng, 3000, 4, 4, 16, 2)
+    books[0, 3] = 3e25
+    dev = icqb.DeviceIndex(books, codes, fast)
+    Q = rng.standard_normal((3, 4))
+    ids, scores, refine, _ = dev.search_host(Q, 10, 0.0, exact=False)
+    for i in range(3):
+        ref = O.two_step(books, codes, fast, 0.0, Q[i], 10)
+        assert np.array_equal(ids[i], ref.ids)
+        assert np.array_equal(scores[i], ref.scores)
+        assert int(refine[i]) == ref.ops.refinements

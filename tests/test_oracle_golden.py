@@ -68,3 +68,25 @@ def test_pairwise_leaves_cover():
         assert sum(p[2] for p in leaves) == n
         assert all(p[2] <= 128 for p in leaves)
         assert len(prog) == 2 * len(leaves) - 1
+
+
+def test_gathered_row_sum_order_rule():
+    """The order the CUDA kernels mirror (icq_device.cuh ref_row_sum): numpy's
+    gathered (n, t) score array (search.py:94) is F-contiguous for n >= 2, so
+    rows accumulate sequentially in book order; for n == 1 it is pairwise."""
+    rng = np.random.default_rng(1)
+    for K in (8, 9, 12, 16):
+        table = rng.standard_normal((K, 256)) ** 2 * 100
+        for n in (1, 2, 3, 17, 1000):
+            codes = rng.integers(0, 256, size=(n, K)).astype(np.uint32)
+            for books in (np.arange(K), np.arange(K)[::2].copy()):
+                g = table[books[None, :], codes[:, books]]
+                got = O.gather(table, codes, books)
+                for i in range(n):
+                    if n == 1:
+                        want = O.pairwise_sum(g[i])
+                    else:
+                        want = 0.0
+                        for x in g[i]:
+                            want += float(x)
+                    assert got[i] == want, (K, n, len(books))

@@ -1,0 +1,168 @@
+"""Seeded synthetic workloads for the BASELINE configs (bench / test infrastructure).
+
+BASELINE.json names no public dataset; each config is a seeded synthetic
+distribution with the stated shapes.  Seeds are fixed here
+and recorded in every bench line:
+
+    mixture means / training sample : numpy default_rng(SEED_MEANS / SEED_TRAIN)
+    database rows                   : torch CUDA generator SEED_DB + chunk index
+    queries                         : torch CUDA generator SEED_QUERIES
+
+Codebooks are trained by the reference (tools/train_books.py, run in the build
+container) and committed under bench_data/.  The database is encoded on the
+GPU by ``encode_icm`` — a torch restatement of the reference encoder
+``assign_codes`` (train.py:196-243: greedy residual build-up, then ICM sweeps
+that re-pick one book's code with the others fixed, strict improvement only),
+used here only to prepare bench data (the native CUDA encoder is the next
+scope row).  fp32 matmuls (TF32 off) in place of the reference's fp64 BLAS.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+BOOKS_DIR = ROOT / "bench_data"
+
+SEED_MEANS = 0
+SEED_TRAIN = 1
+SEED_DB = 1000
+SEED_QUERIES = 7
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    n: int
+    d: int
+    K: int
+    F: int
+    Q: int
+    k: int
+    batch: int
+    dist: str
+    comps: int = 0
+    std: float = 0.0
+    train_n: int = 0  # BASELINE's stated training sample (we train on a recorded subsample)
+
+
+CONFIGS = {
+    "c1": Workload("c1", 100_000, 128, 8, 2, 1000, 10, 1000, "gmm", 32, 0.3, 100_000),
+    "c2": Workload("c2", 1_000_000, 128, 8, 2, 10_000, 100, 10_000, "lognormal", train_n=100_000),
+    "c3": Workload("c3", 1_000_000, 960, 16, 4, 1000, 10, 1000, "gamma", train_n=100_000),
+    "c4": Workload("c4", 10_000_000, 128, 16, 4, 10_000, 100, 256, "gmm", 256, 0.25, 200_000),
+    "c5": Workload("c5", 100_000_000, 96, 8, 2, 10_000, 100, 512, "gmm", 1024, 0.2, 1_000_000),
+}
+
+
+def mixture_means(w: Workload) -> np.ndarray | None:
+    if w.dist != "gmm":
+        return None
+    return np.random.default_rng(SEED_MEANS).standard_normal((w.comps, w.d))
+
+
+def sample_numpy(w: Workload, n: int, rng: np.random.Generator) -> np.ndarray:
+    """Host sample of the config's distribution (used to train the books)."""
+    if w.dist == "gmm":
+        means = mixture_means(w)
+        lab = rng.integers(0, w.comps, size=n)
+        return (means[lab] + w.std * rng.standard_normal((n, w.d))).astype(np.float32)
+    if w.dist == "lognormal":
+        return np.round(np.clip(np.exp(rng.normal(2.0, 1.0, size=(n, w.d))), 0, 255)).astype(
+            np.float32)
+    if w.dist == "gamma":
+        return np.clip(rng.gamma(2.0, 0.05, size=(n, w.d)), 0.0, 1.0).astype(np.float32)
+    raise ValueError(w.dist)
+
+
+def sample_torch(w: Workload, n: int, seed: int, device="cuda"):
+    """Device sample of the config's distribution (database rows / queries)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    if w.dist == "gmm":
+        means = torch.from_numpy(mixture_means(w)).to(device=device, dtype=torch.float32)
+        lab = torch.randint(0, w.comps, (n,), generator=g, device=device)
+        return means[lab] + w.std * torch.randn((n, w.d), generator=g, device=device)
+    if w.dist == "lognormal":
+        x = torch.randn((n, w.d), generator=g, device=device) + 2.0
+        return torch.round(torch.clamp(torch.exp(x), 0, 255))
+    if w.dist == "gamma":
+        # Gamma(shape=2, scale=0.05) = 0.05 * (E1 + E2), E ~ Exp(1)
+        u = torch.rand((2, n, w.d), generator=g, device=device).clamp_min_(1e-12)
+        x = -0.05 * torch.log(u).sum(0)
+        return torch.clamp(x, 0.0, 1.0)
+    raise ValueError(w.dist)
+
+
+def load_books(w: Workload):
+    z = np.load(BOOKS_DIR / f"books_{w.name}.npz", allow_pickle=False)
+    meta = {k: z[k].item() if z[k].ndim == 0 else z[k] for k in z.files if k != "books"}
+    return z["books"].astype(np.float32), meta
+
+
+def encode_icm(x, books, sweeps: int = 10, chunk: int = 1 << 21):
+    """(n, d) float32 cuda tensor -> (n, K) uint8 codes (greedy + ICM, train.py:196-243)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        B = torch.as_tensor(books, device=x.device, dtype=torch.float32)  # (K, m, d)
+        K, m, _ = B.shape
+        c_sq = (B * B).sum(-1)  # (K, m)
+        out = torch.empty((x.shape[0], K), dtype=torch.uint8, device=x.device)
+        for s in range(0, x.shape[0], chunk):
+            xs = x[s:s + chunk]
+            rows = torch.arange(xs.shape[0], device=x.device)
+            codes = torch.empty((xs.shape[0], K), dtype=torch.int64, device=x.device)
+            res = xs.clone()
+            for b in range(K):
+                dist = c_sq[b][None, :] - 2.0 * (res @ B[b].T)
+                codes[:, b] = dist.argmin(1)
+                res -= B[b][codes[:, b]]
+            recon = xs - res
+            for _ in range(sweeps):
+                changed = 0
+                for b in range(K):
+                    cur = codes[:, b]
+                    target = xs - (recon - B[b][cur])
+                    dist = c_sq[b][None, :] - 2.0 * (target @ B[b].T)
+                    best = dist.argmin(1)
+                    imp = dist[rows, best] < dist[rows, cur]
+                    hit = imp.nonzero().squeeze(1)
+                    if hit.numel():
+                        recon[hit] += B[b][best[hit]] - B[b][cur[hit]]
+                        codes[hit, b] = best[hit]
+                        changed += hit.numel()
+                if changed == 0:
+                    break
+            out[s:s + chunk] = codes.to(torch.uint8)
+        return out
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def build_database(w: Workload, books, sweeps: int = 4, chunk_rows: int = 1 << 22,
+                   device="cuda"):
+    """Generate the config's database chunk by chunk on the GPU, encode it, and
+    keep only the uint8 codes (n, K) on the device."""
+    import torch
+
+    codes = torch.empty((w.n, w.K), dtype=torch.uint8, device=device)
+    for ci, s in enumerate(range(0, w.n, chunk_rows)):
+        e = min(w.n, s + chunk_rows)
+        x = sample_torch(w, e - s, SEED_DB + ci, device)
+        codes[s:e] = encode_icm(x, books, sweeps=sweeps)
+        del x
+    return codes
+
+
+def queries(w: Workload, device="cuda"):
+    import torch
+
+    return sample_torch(w, w.Q, SEED_QUERIES, device).to(torch.float64)
