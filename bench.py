@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""ICQ query-path benchmark on B200 — prints ONE JSON line (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
+
+Workload: one BASELINE config (default c2 = configs[1]; c1..c5 selectable),
+seeded synthetic data (tools/workloads.py), books trained by the reference
+(bench_data/), database encoded on the GPU.  A step = one batch of queries
+through the hot path (K1 LUT build + fused scan/prune/refine/top-k kernel).
+
+value    queries/s over all ranks, device time (CUDA events on the launch
+         stream), inputs resident in HBM, L2 flushed before every step
+e2e      queries/s through the C-ABI host-buffer call (icq_search_host):
+         pinned host queries -> H2D -> search -> D2H of ids/scores/refinements
+roofline effective code-stream bandwidth of the scan kernel:
+         (batch * n * |F| fast-code bytes) / scan-kernel time, vs the measured
+         HBM copy peak (MEASURED_PEAKS.json)
+cpu_baseline the reference algorithm's CPU port (oracle.two_step_loop, a
+         literal restatement of search.py:112-165) on a bounded query sample,
+         all host cores, rank 0 at N=1.
+Multi-GPU: query batches are independent -> replicas, no collective
+(scaling "weak": each rank runs the same number of batches).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from tools.workloads import CONFIGS, SEED_DB, SEED_QUERIES, SEED_TRAIN  # noqa: E402
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        z = json.loads(p.read_text())
+        return float(z["hbm_gbs"]), float(z.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference algorithm on host cores
+# ---------------------------------------------------------------------------
+_CPU = {}
+
+
+def _cpu_one(qi):
+    from oracle import icq_oracle as O
+
+    c = _CPU
+    t0 = time.perf_counter()
+    r = O.two_step_loop(c["books"], c["codes"], c["fast"], c["sigma"], c["Q"][qi], c["k"])
+    return qi, r.ids, r.scores, r.ops.refinements, time.perf_counter() - t0
+
+
+def cpu_baseline(books, codes_host, fast, sigma, Qhost, k, nq, workers):
+    import multiprocessing as mp
+
+    _CPU.update(books=books, codes=codes_host, fast=fast, sigma=sigma, Q=Qhost, k=k)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_one, range(nq), chunksize=1)
+    wall = time.perf_counter() - t0
+    return res, wall
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c2"),
+                    choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--sigma", type=float, default=None, help="override the learned margin")
+    ap.add_argument("--sweeps", type=int, default=10, help="ICM sweeps when encoding the database")
+    ap.add_argument("--cpu-queries", type=int, default=0, help="CPU baseline sample (0 = auto)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference" and rank != 0:
+        return 0  # the CPU reference arm runs on rank 0 only
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1 and args.impl == "b200":
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from tools.workloads import build_database, load_books, queries
+
+    w = CONFIGS[args.config]
+    books, meta = load_books(w)
+    learned_fast = np.asarray(meta["learned_fast"], dtype=np.uint32)
+    if learned_fast.size == w.F:
+        fast, rule = learned_fast, "learned"
+    else:
+        fast, rule = np.arange(w.F, dtype=np.uint32), "first-F (SURVEY 8d: learned fast set %s)" % (
+            learned_fast.tolist())
+    sigma = float(meta["learned_sigma"]) if args.sigma is None else float(args.sigma)
+
+    t0 = time.time()
+    codes = build_database(w, books, sweeps=args.sweeps)
+    Qall = queries(w)
+    torch.cuda.synchronize()
+    prep_s = time.time() - t0
+    B = w.batch
+    nbatches = (w.Q + B - 1) // B
+
+    base_config = {
+        "workload": f"{w.name}: n={w.n} d={w.d} K={w.K} m=256 |F|={w.F} k={w.k} "
+                    f"queries={w.Q} batch={B} dist={w.dist}",
+        "n": w.n, "d": w.d, "K": w.K, "m": 256, "F": w.F, "k": w.k, "batch": B,
+        "fast": fast.tolist(), "fast_rule": rule, "sigma": sigma,
+        "books": f"reference icq.train on {int(meta['train_rows'])} seeded rows, "
+                 f"{int(meta['epochs'])} epoch(s), seed {int(meta['seed'])}",
+        "seeds": {"train": SEED_TRAIN, "db": SEED_DB, "queries": SEED_QUERIES},
+        "encode": f"GPU ICM (greedy + <= {args.sweeps} sweeps, fp32)",
+        "l2": "flushed (256 MiB write) before every timed step",
+        "parallelism": f"replicas{world}" if world > 1 else "single",
+    }
+
+    if args.impl == "reference":
+        return run_reference(args, w, books, codes, fast, sigma, Qall, base_config)
+
+    import paper_1912_08756_b200 as icqb
+
+    dev = icqb.DeviceIndex.from_device(books, codes, fast)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def batch(i):
+        b = (rank + i * world) % nbatches
+        return Qall[b * B:(b + 1) * B]
+
+    def step(i, ev=None):
+        qb = batch(i)
+        flush.zero_()
+        if ev:
+            ev[0].record(stream)
+        lut = dev.build_lut_device(qb)
+        if ev:
+            ev[1].record(stream)
+        out = dev.search_lut_device(lut, w.k, sigma, stats=True)
+        if ev:
+            ev[2].record(stream)
+        return qb.shape[0], out
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    outs = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            outs.append(step(args.warmup + i, evs[i]))
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_lut = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
+    t_scan = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
+    t_total = t_lut + t_scan
+    nq = sum(o[0] for o in outs)
+    refine = torch.cat([o[1]["refinements"] for o in outs]).double()
+    stats = torch.cat([o[1]["stats"] for o in outs]).double()
+    if dist:
+        tt = torch.tensor([t_total, t_scan, t_lut], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total, t_scan, t_lut = tt.tolist()
+        nqt = torch.tensor([nq], dtype=torch.float64, device="cuda")
+        dist.all_reduce(nqt)
+        nq_all = int(nqt.item())
+    else:
+        nq_all = nq
+    qps = nq_all / t_total
+    lookups = nq * w.n * w.F
+    scan_gbs = lookups / t_scan / 1e9  # per-GPU scan kernel (this rank)
+    hbm_peak, sm_max, peak_kind = _peaks()
+    smem_peak_glps = 148 * 32 * sm_max * 1e6 / 1e9
+
+    # e2e through the C-ABI host-buffer call (pinned host queries)
+    e2e = None
+    if not args.no_e2e:
+        Qpin = torch.empty((B, w.d), dtype=torch.float64, pin_memory=True)
+        e2e_t = 0.0
+        e2e_n = 0
+        for i in range(args.warmup + args.steps):
+            qb = batch(i)
+            Qpin[:qb.shape[0]].copy_(qb.cpu())
+            qh = Qpin[:qb.shape[0]].numpy()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dev.search_host(qh, w.k, sigma, exact=False)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                e2e_t += dt
+                e2e_n += qb.shape[0]
+        e2e_rate = e2e_n / e2e_t
+        if dist:
+            tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_rate = e2e_n * world / tt.item()
+        e2e = {"value": e2e_rate, "unit": "queries/s", "h2d_bytes_per_step": B * w.d * 8,
+               "d2h_bytes_per_step": B * w.k * 16 + B * 8,
+               "path": "icq_search_host (C ABI, host buffers)"}
+
+    # recall of two-step vs exact engine + parity sample vs the CPU reference port
+    qb = batch(0)
+    two = dev.search_device(qb, w.k, sigma)
+    ex = dev.search_device(qb, w.k, exact=True)
+    torch.cuda.synchronize()
+    ti, ei = two["ids"].cpu().numpy(), ex["ids"].cpu().numpy()
+    recall = float(np.mean([np.isin(ti[i], ei[i]).mean() for i in range(ti.shape[0])]))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        codes_h = codes.cpu().numpy()
+        nqc = args.cpu_queries or max(8, min(64, int(2.0e8 // max(1, w.n * w.K))))
+        workers = min(os.cpu_count() or 1, nqc)
+        if w.n >= 50_000_000:
+            workers = min(workers, 2)  # ~10-17 GB of temporaries per in-flight query
+        Qh = Qall[:nqc].cpu().numpy()
+        res, wall = cpu_baseline(books, codes_h, fast, sigma, Qh, w.k, nqc, workers)
+        ids, sc, rf, _ = dev.search_host(Qh, w.k, sigma, exact=False)
+        mism = sum(int(not (np.array_equal(ids[qi], r_ids) and np.array_equal(sc[qi], r_sc)
+                            and rf[qi] == r_rf)) for qi, r_ids, r_sc, r_rf, _ in res)
+        cpu = {"value": nqc / wall, "unit": "queries/s", "cores": workers, "kind": "port",
+               "sample": f"{nqc} queries of {w.name} (first {nqc} of the query set), oracle."
+                         f"two_step_loop (literal search.py:112-165), {workers} processes",
+               "cpu_seconds": sum(r[4] for r in res),
+               "parity_vs_gpu": {"queries": nqc, "mismatches": mism}}
+
+    line = {
+        "metric": "queries/sec (top-k two-step ICQ search); G code-lookups/s; fast-scan GB/s vs roofline",
+        "value": qps,
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_total / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 codes / f32 scan / f64 certified scores",
+        "data": "synthetic (seeded; BASELINE names no dataset)",
+        "config": base_config,
+        "glookups_per_s": nq_all * w.n * w.F / t_total / 1e9,
+        "lut_ms_per_step": t_lut / args.steps * 1e3,
+        "scan_ms_per_step": t_scan / args.steps * 1e3,
+        "pruning": {"refined_fraction": float(refine.mean().item() / w.n),
+                    "insertions_per_query": float(stats[:, 0].mean().item()),
+                    "replay_candidates_per_query": float(stats[:, 1].mean().item()),
+                    "f64_certified_per_query": float(stats[:, 2].mean().item()),
+                    "prologue_items_per_query": float(stats[:, 3].mean().item()),
+                    "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
+                    "phase2_cycles_per_query": float(stats[:, 5].mean().item()),
+                    "replay_wait_cycles_per_query": float(stats[:, 6].mean().item()),
+                    "wide_queries": int(stats[:, 7].sum().item()),
+                    "recall_vs_exact": recall},
+        "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": scan_gbs / hbm_peak, "traffic": None,
+                     "peak_kind": peak_kind,
+                     "kernel": "icq_scan_kernel (K2-K5 fused)",
+                     "algorithmic_bytes_per_launch": B * w.n * w.F,
+                     "smem_gather_frac": (lookups / t_scan / 1e9) / smem_peak_glps},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps,
+        "cpu_baseline": cpu,
+        "setup_seconds": prep_s,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_reference(args, w, books, codes, fast, sigma, Qall, base_config):
+    """--impl reference: the reference algorithm's CPU port on host cores."""
+    codes_h = codes.cpu().numpy()
+    nq = args.cpu_queries or max(8, min(32, int(1.0e8 // max(1, w.n * w.K))))
+    workers = min(os.cpu_count() or 1, nq)
+    if w.n >= 50_000_000:
+        workers = min(workers, 2)
+    Qh = Qall.cpu().numpy()
+    rates = []
+    for i in range(args.warmup + args.steps):
+        sel = Qh[(i * nq) % w.Q:(i * nq) % w.Q + nq]
+        res, wall = cpu_baseline(books, codes_h, fast, sigma, sel, w.k, sel.shape[0], workers)
+        if i >= args.warmup:
+            rates.append((sel.shape[0], wall))
+    tot_q = sum(r[0] for r in rates)
+    tot_t = sum(r[1] for r in rates)
+    v = tot_q / tot_t
+    line = {
+        "impl": "reference",
+        "metric": "queries/sec (top-k two-step ICQ search); G code-lookups/s; fast-scan GB/s vs roofline",
+        "value": v, "unit": "queries/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded)", "config": base_config,
+        "cpu_baseline": {"value": v, "unit": "queries/s", "cores": workers, "kind": "port",
+                         "sample": f"{nq} queries per step, oracle.two_step_loop "
+                                   f"(literal search.py:112-165), {workers} processes"},
+        "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -99,9 +99,11 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
  *   refine_dev   : int64 [Q]     ops.refinements (search.py:160); may be NULL
  *   survivors_dev: optional uint32 bitmap [Q * ceil(n/32)] of refined ids
  *                  (instrumentation for parity tests; NULL to skip)
- *   stats_dev    : optional int64 [Q*4] diagnostics per query: heap insertions,
+ *   stats_dev    : optional int64 [Q*8] diagnostics per query: heap insertions,
  *                  items examined by the in-order replay, items certified in
- *                  float64 (near-ties of the fp32 filter), replayed groups
+ *                  float64 (near-ties of the fp32 filter), end of the dense
+ *                  prologue (item id), prologue cycles, phase-2 cycles,
+ *                  replay cycles spent waiting for the scan, wide-mode flag
  *   fallback_out : optional host int32; set to 1 when the fast set is empty and
  *                  the exact engine ran instead (search.py:127-131)
  * The call is asynchronous on `stream` (no host synchronisation).
@@ -116,6 +118,14 @@ icq_status icq_search_two_step(icq_index_t h, const double* q_dev, int32_t Q, in
 icq_status icq_search_exact(icq_index_t h, const double* q_dev, int32_t Q, int32_t k,
                             int64_t* ids_dev, double* scores_dev,
                             void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* Same two engines on a precomputed float64 LUT (icq_build_lut output,
+ * dev float64 [Q*K*m]); no workspace.  exact = 1 runs search_exact.  Lets a
+ * caller reuse tables across calls and time the scan kernel on its own. */
+icq_status icq_search_with_lut(icq_index_t h, const double* lut_dev, int32_t Q, int32_t k,
+                               double sigma, int32_t exact, int64_t* ids_dev, double* scores_dev,
+                               int64_t* refine_dev, uint32_t* survivors_dev, int64_t* stats_dev,
+                               int32_t* fallback_out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Host-buffer entry points (end-to-end: H2D of queries, search, D2H of results,

@@ -39,6 +39,8 @@ SIGNATURES = {
     "icq_search_two_step": (_i32, [_vp, _vp, _i32, _i32, C.c_double, _vp, _vp, _vp, _vp, _vp,
                                    C.POINTER(_i32), _vp, C.c_size_t, _vp]),
     "icq_search_exact": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "icq_search_with_lut": (_i32, [_vp, _vp, _i32, _i32, C.c_double, _i32, _vp, _vp, _vp, _vp,
+                                   _vp, C.POINTER(_i32), _vp]),
     "icq_search_host": (_i32, [_vp, _vp, _i32, _i32, C.c_double, _i32, _vp, _vp, _vp,
                                C.POINTER(_i32)]),
 }

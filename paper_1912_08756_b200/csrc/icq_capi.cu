@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -47,6 +48,10 @@ struct icq_index_s {
   LutProg* prog_dev;
   int32_t* err_dev;
   int64_t bytes;
+  // device scratch of the synchronous host-buffer path, reused across calls
+  std::mutex host_mu;
+  char* host_buf = nullptr;
+  size_t host_buf_bytes = 0;
 };
 
 static int pow2_ceil(int x) {
@@ -213,6 +218,7 @@ icq_status icq_index_destroy(icq_index_t h) {
   if (!h->fast_alias) cudaFree(h->codes_fast);
   cudaFree(h->prog_dev);
   cudaFree(h->err_dev);
+  cudaFree(h->host_buf);
   delete h;
   return ICQ_OK;
 }
@@ -244,10 +250,10 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
   return ICQ_OK;
 }
 
-static icq_status search_impl(icq_index_t h, const double* q, int32_t Q, int32_t k, double sigma,
-                              bool exact, int64_t* ids, double* scores, int64_t* refine,
-                              uint32_t* survivors, int64_t* stats, int32_t* fallback_out,
-                              void* ws, size_t ws_bytes, cudaStream_t s) {
+static icq_status search_impl(icq_index_t h, const double* q, const double* lut_in, int32_t Q,
+                              int32_t k, double sigma, bool exact, int64_t* ids, double* scores,
+                              int64_t* refine, uint32_t* survivors, int64_t* stats,
+                              int32_t* fallback_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
   if (!(k >= 1 && (int64_t)k <= h->n))
     return fail(ICQ_ERR_VALIDATION, "k=%d out of range [1, %lld]", k, (long long)h->n);
@@ -257,12 +263,16 @@ static icq_status search_impl(icq_index_t h, const double* q, int32_t Q, int32_t
   if (fallback_out) *fallback_out = fallback ? 1 : 0;
   if (fallback) exact = true;
   if (Q == 0) return ICQ_OK;
-  size_t need = 0;
-  icq_workspace_size(h, Q, k, &need);
-  if (!ws || ws_bytes < need)
-    return fail(ICQ_ERR_NOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, need);
-  double* lut = reinterpret_cast<double*>(ws);
-  CUDA_TRY(launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, s));
+  const double* lut = lut_in;
+  if (!lut) {
+    size_t need = 0;
+    icq_workspace_size(h, Q, k, &need);
+    if (!ws || ws_bytes < need)
+      return fail(ICQ_ERR_NOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+    double* w = reinterpret_cast<double*>(ws);
+    CUDA_TRY(launch_lut(h->books, q, w, h->K, h->m, h->d, Q, h->prog_dev, s));
+    lut = w;
+  }
   if (survivors) {
     const int64_t words = (h->n + 31) / 32;
     CUDA_TRY(cudaMemsetAsync(survivors, 0, (size_t)Q * words * sizeof(uint32_t), s));
@@ -273,7 +283,8 @@ static icq_status search_impl(icq_index_t h, const double* q, int32_t Q, int32_t
   p.lut64 = lut;
   p.ids = ids;
   p.scores = scores;
-  p.refinements = exact ? nullptr : refine;
+  p.refinements = refine;
+  p.exact_mode = exact ? 1 : 0;
   p.survivors = exact ? nullptr : survivors;
   p.stats = stats;
   p.error = h->err_dev;
@@ -302,13 +313,6 @@ static icq_status search_impl(icq_index_t h, const double* q, int32_t Q, int32_t
   if (unsupported)
     return fail(ICQ_ERR_UNSUPPORTED, "k=%d does not fit the on-chip heap for K=%d, m=%d", k, h->K,
                 h->m);
-  if (exact && refine) {
-    // search_exact reports refinements = n (search.py:108)
-    std::vector<int64_t> nn((size_t)Q, h->n);
-    CUDA_TRY(cudaMemcpyAsync(refine, nn.data(), (size_t)Q * sizeof(int64_t),
-                             cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-  }
   return ICQ_OK;
 }
 
@@ -316,14 +320,23 @@ icq_status icq_search_two_step(icq_index_t h, const double* q, int32_t Q, int32_
                                int64_t* ids, double* scores, int64_t* refine, uint32_t* survivors,
                                int64_t* stats, int32_t* fallback_out, void* ws, size_t ws_bytes,
                                void* stream) {
-  return search_impl(h, q, Q, k, sigma, false, ids, scores, refine, survivors, stats,
+  return search_impl(h, q, nullptr, Q, k, sigma, false, ids, scores, refine, survivors, stats,
                      fallback_out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 icq_status icq_search_exact(icq_index_t h, const double* q, int32_t Q, int32_t k, int64_t* ids,
                             double* scores, void* ws, size_t ws_bytes, void* stream) {
-  return search_impl(h, q, Q, k, 0.0, true, ids, scores, nullptr, nullptr, nullptr, nullptr, ws,
-                     ws_bytes, (cudaStream_t)stream);
+  return search_impl(h, q, nullptr, Q, k, 0.0, true, ids, scores, nullptr, nullptr, nullptr,
+                     nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+icq_status icq_search_with_lut(icq_index_t h, const double* lut_dev, int32_t Q, int32_t k,
+                               double sigma, int32_t exact, int64_t* ids_dev, double* scores_dev,
+                               int64_t* refine_dev, uint32_t* survivors_dev, int64_t* stats_dev,
+                               int32_t* fallback_out, void* stream) {
+  if (!lut_dev) return fail(ICQ_ERR_VALIDATION, "lut_dev is NULL");
+  return search_impl(h, nullptr, lut_dev, Q, k, sigma, exact != 0, ids_dev, scores_dev, refine_dev,
+                     survivors_dev, stats_dev, fallback_out, nullptr, 0, (cudaStream_t)stream);
 }
 
 icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32_t k,
@@ -343,9 +356,16 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
   const size_t ib = (size_t)Q * k * sizeof(int64_t);
   const size_t sb = (size_t)Q * k * sizeof(double);
   const size_t rb = (size_t)Q * sizeof(int64_t);
-  char* buf = nullptr;
   const size_t total = ws_bytes + qb + ib + sb + rb + 4 * 256;
-  CUDA_TRY(cudaMallocAsync((void**)&buf, total, s));
+  std::lock_guard<std::mutex> guard(h->host_mu);
+  if (h->host_buf_bytes < total) {
+    cudaFree(h->host_buf);
+    h->host_buf = nullptr;
+    h->host_buf_bytes = 0;
+    CUDA_TRY(cudaMalloc((void**)&h->host_buf, total));
+    h->host_buf_bytes = total;
+  }
+  char* buf = h->host_buf;
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   char* ws = buf;
   double* qd = reinterpret_cast<double*>(buf + al(ws_bytes));
@@ -355,8 +375,8 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
   icq_status st = ICQ_OK;
   cudaError_t e = cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) {
-    st = search_impl(h, qd, Q, k, sigma, exact != 0, idd, scd, rfd, nullptr, nullptr, nullptr, ws,
-                     ws_bytes, s);
+    st = search_impl(h, qd, nullptr, Q, k, sigma, exact != 0, idd, scd, rfd, nullptr, nullptr,
+                     nullptr, ws, ws_bytes, s);
     if (st == ICQ_OK) {
       e = cudaMemcpyAsync(ids_host, idd, ib, cudaMemcpyDeviceToHost, s);
       if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, sb, cudaMemcpyDeviceToHost, s);
@@ -364,7 +384,6 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
         e = cudaMemcpyAsync(refine_host, rfd, rb, cudaMemcpyDeviceToHost, s);
     }
   }
-  cudaFreeAsync(buf, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (st != ICQ_OK) return st;
   if (e != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e));

@@ -10,28 +10,38 @@
 // search_exact (:97-109) is the same kernel with the fast set = all books and
 // sigma = 0 (then fast == exact and the prune predicate is the top-k test).
 //
-// CTA layout (288 threads, one CTA per SM, persistent over the database):
-//   warps 1..8  SCAN   stream the fast-code column block (16-byte loads,
-//                      register double-prefetch), gather |F| float32 entries
-//                      per item from lane-private replicated LUT pages
-//                      (conflict-free: entry j of book s for lane l sits in
-//                      bank l; its address is ONE byte_perm of the code word),
-//                      and publish per-item fast scores + per-group minima
-//                      into a ring of segment slots.
-//   warp 0      REPLAY consumes slots strictly in database order against the
-//                      LIVE bound: groups whose minimum clears the bound are
-//                      expanded, candidates are decided with certified float32
-//                      thresholds (float64 recomputation only for near-ties),
-//                      refined items are scored exactly in float64 from the
-//                      shared float64 LUT, and insertions update a sorted heap
-//                      in shared memory.  The result is bitwise the reference's.
-// Slots are handed over with mbarriers (full: 256 scan-thread arrivals;
-// empty: 32 replay-lane arrivals).
+// One CTA (288 threads, one per SM) owns one query and walks the database in
+// order in two phases:
+//
+// Phase 1 — dense prologue (insertion-heavy start, ~k*ln(i/k) insertions).
+//   All 9 warps score chunks of items exactly in float64 (rows from HBM, the
+//   float64 LUT in shared memory); warp 0 then replays the reference loop
+//   over the chunk with float64 compares only.  Runs until a whole segment
+//   sees few insertions.
+//
+// Phase 2 — pipelined scan (the streaming hot path).
+//   warps 1..8 SCAN   stream the fast-code block (16-byte loads, two segments
+//                     of register prefetch), gather |F| float32 entries per item
+//                     from lane-private replicated LUT pages (conflict-free:
+//                     entry j of book s for lane l sits in bank l; its address
+//                     is ONE byte_perm of the code word), publish per-item fast
+//                     scores and per-group / per-warp minima into a ring of
+//                     segment slots, and for items under the replay's published
+//                     prefetch threshold fetch the full code row (cp.async) and
+//                     precompute the float64 fast and exact scores one segment
+//                     later — so the order-independent work never waits.
+//   warp 0     REPLAY consumes slots strictly in database order against the
+//                     LIVE bound: warps/groups whose minimum clears the bound
+//                     are expanded 32 items at a time, candidates are decided
+//                     with certified float32 thresholds (float64 only for
+//                     near-ties), insertions update a sorted heap in shared
+//                     memory.  Everything it compares is float64 and bitwise
+//                     the reference's.
+//   Slots are handed over with mbarriers (full: 256 scan-thread arrivals
+//   after the cp.async rows landed; empty: 32 replay-lane arrivals).
 #include "icq_types.cuh"
 
 namespace icq {
-
-
 
 template <int FP>
 struct Geo {
@@ -40,11 +50,14 @@ struct Geo {
   static constexpr int P = (FP + BPR - 1) / BPR;                 // 64 KiB pages
   static constexpr int IPC = 16 / FP;                            // items per 16-B chunk
   static constexpr int S = kNC * IPC;                            // items per segment
-  static constexpr uint32_t slot_bytes = (IPC * kValStride + kNC) * 4;
 };
 
+constexpr int kPubR = 3;             // prefetch threshold covers the next kPubR insertions
+constexpr int kDenseStopIns = 6;     // leave the prologue once a segment sees <= this many
+#define kInf (__int_as_float(0x7f800000))
+
 // --------------------------------------------------------------------------
-// float64 scores in the reference's order (search.py:94 -> numpy pairwise)
+// float64 scores in the reference's order (search.py:94, see ref_row_sum)
 // --------------------------------------------------------------------------
 struct Row {
   uint32_t w[4];
@@ -74,6 +87,21 @@ __device__ __forceinline__ Row load_row(const uint8_t* codes_full, int KP, int64
   return r;
 }
 
+__device__ __forceinline__ Row smem_row(const uint8_t* p, int KP) {
+  Row r;
+  r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0;
+  if (KP == 16) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    r.w[0] = v.x; r.w[1] = v.y; r.w[2] = v.z; r.w[3] = v.w;
+  } else if (KP == 8) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    r.w[0] = v.x; r.w[1] = v.y;
+  } else {
+    r.w[0] = *reinterpret_cast<const uint32_t*>(p);
+  }
+  return r;
+}
+
 __device__ __forceinline__ double exact64(const double* lut, int m, int K, bool pw, const Row& r) {
   return ref_row_sum(K, pw, [&](int b) { return lut[b * m + (int)r.byte(b)]; });
 }
@@ -95,6 +123,7 @@ __device__ __forceinline__ bool key_gt(double e1, int32_t i1, double e2, int32_t
 __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, double e, int32_t id,
                                  double f, int lane) {
   int g = 0;
+#pragma unroll 4
   for (int base = 1; base < k; base += 32) {
     const int i = base + lane;
     const bool gt = i < k && key_gt(he[i], hi[i], e, id);
@@ -113,14 +142,263 @@ __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, dou
   __syncwarp();
 }
 
+// The replay warp's view of the heap: the k best (exact, id) entries sorted
+// descending (entry 0 = heap maximum, search.py:140).  For k <= 128 the
+// entries live in warp-0 registers (entry i = r*32 + lane) so an insertion is
+// a handful of ballots and shuffles; larger k falls back to shared memory.
+constexpr int kRegHeapRegs = 4;
+struct WarpHeap {
+  int k;
+  bool reg;
+  double e[kRegHeapRegs], f[kRegHeapRegs];
+  int32_t id[kRegHeapRegs];
+  double* he;
+  double* hf;
+  int32_t* hi;
+
+  __device__ __forceinline__ void load(int lane) {
+    if (!reg) return;
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = r * 32 + lane;
+      e[r] = i < k ? he[i] : 0.0;
+      f[r] = i < k ? hf[i] : 0.0;
+      id[r] = i < k ? hi[i] : 0;
+    }
+  }
+  __device__ __forceinline__ void store(int lane) {
+    if (!reg) return;
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = r * 32 + lane;
+      if (i < k) { he[i] = e[r]; hf[i] = f[r]; hi[i] = id[r]; }
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ double top_e() const {
+    return reg ? __shfl_sync(0xffffffffu, e[0], 0) : he[0];
+  }
+  __device__ __forceinline__ double top_f() const {
+    return reg ? __shfl_sync(0xffffffffu, f[0], 0) : hf[0];
+  }
+  // max fast score over entries 0..R (R < 32)
+  __device__ __forceinline__ double top_fast_max(int R, int lane) const {
+    double a = (lane <= R && lane < k) ? (reg ? f[0] : hf[lane]) : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    return a;
+  }
+  __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
+    if (!reg) {
+      heap_replace_max(he, hf, hi, k, xe, xid, xf, lane);
+      return;
+    }
+    int g = 0;  // entries 1..k-1 that stay above x
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = r * 32 + lane;
+      g += __popc(__ballot_sync(0xffffffffu, i >= 1 && i < k && key_gt(e[r], id[r], xe, xid)));
+    }
+    // new[i] = old[i+1] for i < g, x at g, unchanged above
+    double se[kRegHeapRegs], sf[kRegHeapRegs];
+    int32_t si[kRegHeapRegs];
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int rn = r + 1 < kRegHeapRegs ? r + 1 : r;
+      const double de = __shfl_down_sync(0xffffffffu, e[r], 1);
+      const double df = __shfl_down_sync(0xffffffffu, f[r], 1);
+      const int32_t di = __shfl_down_sync(0xffffffffu, id[r], 1);
+      const double ne = __shfl_sync(0xffffffffu, e[rn], 0);
+      const double nf = __shfl_sync(0xffffffffu, f[rn], 0);
+      const int32_t ni = __shfl_sync(0xffffffffu, id[rn], 0);
+      se[r] = lane == 31 ? ne : de;
+      sf[r] = lane == 31 ? nf : df;
+      si[r] = lane == 31 ? ni : di;
+    }
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = r * 32 + lane;
+      if (i < g) { e[r] = se[r]; f[r] = sf[r]; id[r] = si[r]; }
+      else if (i == g) { e[r] = xe; f[r] = xf; id[r] = xid; }
+    }
+  }
+};
+
+// cp.async helpers (rows of candidate items into the slot)
+__device__ __forceinline__ void cp_async_row(uint32_t dst, const void* src, int bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // --------------------------------------------------------------------------
-// SCAN warps
+// shared context
+// --------------------------------------------------------------------------
+struct Ctx {
+  const ScanParams* p;
+  uint8_t* dsm;
+  uint32_t dbase;
+  double* lut;  // float64 LUT [K][m]
+  double* he;
+  double* hf;
+  int32_t* hi;
+  uint32_t ctrl;
+  bool pw;
+  bool wide;
+  __device__ __forceinline__ uint8_t* at(uint32_t abs) const { return dsm + (abs - dbase); }
+};
+
+// ctrl block: [0,32) full[4]  [32,64) empty[4]  [64,96) counters  96 pub_thr
+//             100 prologue flag  104 int64 phase-2 start item
+constexpr uint32_t kCtrlBytes = 128;
+
+// Replay state (warp 0 only; warp-uniform registers)
+struct Live {
+  double T64, bound64, thr64;
+  float lo, hi;
+  int64_t refinements, insertions, candidates, certified;
+  int64_t wait_cycles;  // replay time spent waiting for the scan warps
+  WarpHeap H;
+};
+
+__device__ __forceinline__ void live_update(Live& L, const Ctx& c, int F, double sigma, bool wide,
+                                           int k, int lane) {
+  L.T64 = L.H.top_e();
+  L.bound64 = L.H.top_f();
+  L.thr64 = __dadd_rn(L.bound64, sigma);
+  if (wide) {
+    L.lo = -kInf;
+    L.hi = kInf;
+  } else {
+    certified_bounds(L.thr64, F, L.lo, L.hi);
+  }
+  // publish the scan warps' row-prefetch threshold: the bound stays <= the
+  // max fast score over the top kPubR+1 heap entries (+ sigma per insertion)
+  // for the next kPubR insertions.
+  const double a = L.H.top_fast_max(kPubR, lane);
+  float lo2, hi2;
+  certified_bounds(__dadd_rn(a, sigma * (kPubR + 1)), F, lo2, hi2);
+  if (lane == 0) {
+    volatile float* pub = reinterpret_cast<volatile float*>(c.at(c.ctrl + 96));
+    *pub = wide ? kInf : hi2;
+  }
+}
+
+__device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {
+  if (surv) atomicOr(surv + (id >> 5), 1u << (id & 31));
+}
+
+// --------------------------------------------------------------------------
+// Phase 1: dense prologue (all warps score, warp 0 decides in float64)
 // --------------------------------------------------------------------------
 template <int FP>
-__device__ __forceinline__ void scan_role(const ScanParams& p, int w, int lane, uint32_t ctrl) {
+__device__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp, int lane) {
+  using G = Geo<FP>;
+  const ScanParams& p = *c.p;
+  const int64_t n = p.n;
+  const int k = p.k;
+  const int C = p.dense_chunk;
+  double* df = reinterpret_cast<double*>(c.at(p.off_slot[0]));
+  double* de = df + C;
+  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(c.at(c.ctrl + 100));
+  uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
+  int64_t pos = k;
+  int seg_ins = 0;
+  while (pos < n) {
+    const int64_t end = min(n, (pos / C + 1) * C);
+    const int cnt = (int)(end - pos);
+    for (int i0 = 0; i0 < cnt; i0 += kThreads * 8) {
+      Row rows[8];  // issue all row loads first, then score (one memory latency per round)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + tid + r * kThreads;
+        if (i < cnt) rows[r] = load_row(p.codes_full, p.KP, pos + i);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = i0 + tid + r * kThreads;
+        if (i < cnt) {
+          df[i] = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, rows[r]);
+          de[i] = exact64(c.lut, p.m, p.K, c.pw, rows[r]);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int b0 = 0; b0 < cnt; b0 += 32) {
+        const int i = b0 + lane;
+        const bool valid = i < cnt;
+        const double f = valid ? df[i] : 0.0;
+        const double e = valid ? de[i] : 0.0;
+        const int64_t id = pos + i;
+        uint32_t done = 0;
+        for (;;) {
+          const bool refined = valid && !((done >> lane) & 1u) && (f < L.thr64);
+          const bool ins = refined && (e < L.T64);
+          const uint32_t rmask = __ballot_sync(0xffffffffu, refined);
+          const uint32_t imask = __ballot_sync(0xffffffffu, ins);
+          const int first = imask ? __ffs(imask) - 1 : 31;
+          const uint32_t decided = imask ? (0xffffffffu >> (31 - first)) : 0xffffffffu;
+          L.refinements += __popc(rmask & decided);
+          L.candidates += __popc(rmask & decided);
+          if (refined && ((decided >> lane) & 1u)) record_survivor(surv, id);
+          done |= decided;
+          if (!imask) break;
+          const double ne = __shfl_sync(0xffffffffu, e, first);
+          const double nf = __shfl_sync(0xffffffffu, f, first);
+          L.H.replace_max(ne, (int32_t)(pos + b0 + first), nf, lane);
+          live_update(L, c, p.F, p.sigma, c.wide, k, lane);
+          ++L.insertions;
+          ++seg_ins;
+        }
+      }
+      // stop at a segment boundary once the insertion rate has dropped
+      bool more = end < n;
+      if (end % G::S == 0) {
+        if (seg_ins <= kDenseStopIns) more = false;
+        seg_ins = 0;
+      }
+      if (lane == 0) *flag = more ? 1 : 0;
+    }
+    __syncthreads();
+    pos = end;
+    if (!*flag) break;
+    __syncthreads();  // chunk buffers are rewritten next round
+  }
+  return pos;
+}
+
+// --------------------------------------------------------------------------
+// Phase 2, SCAN warps
+// --------------------------------------------------------------------------
+template <int FP>
+__device__ __forceinline__ void scan_finalize(const Ctx& c, int slot, int w, int lane) {
+  const ScanParams& p = *c.p;
+  const uint32_t sb = p.off_slot[slot];
+  const int cnt = *reinterpret_cast<volatile int32_t*>(c.at(sb + p.so_ecnt + 4 * w));
+  const int e0 = w * p.cw;
+  for (int e = lane; e < cnt; e += 32) {
+    const Row r = smem_row(c.at(sb + p.so_erow + (uint32_t)(e0 + e) * 16), p.KP);
+    reinterpret_cast<double*>(c.at(sb + p.so_ef64))[e0 + e] =
+        fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
+    reinterpret_cast<double*>(c.at(sb + p.so_ee64))[e0 + e] = exact64(c.lut, p.m, p.K, c.pw, r);
+  }
+}
+
+template <int FP>
+__device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t seg0) {
   using G = Geo<FP>;
   constexpr int IPC = G::IPC;
   constexpr int S = G::S;
+  const ScanParams& p = *c.p;
   uint32_t L[FP];
 #pragma unroll
   for (int s = 0; s < FP; ++s)
@@ -130,8 +408,9 @@ __device__ __forceinline__ void scan_role(const ScanParams& p, int w, int lane, 
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   const int c0 = w * 64 + lane;  // chunk (group) ids owned by this lane
   const int c1 = c0 + 32;
-  const int64_t seg0 = p.k / S;
   const int64_t nseg = p.nseg;
+  const int rowb = p.KP < 4 ? 4 : p.KP;
+  const volatile float* pub = reinterpret_cast<const volatile float*>(c.at(c.ctrl + 96));
 
   uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
   if (seg0 < nseg) {
@@ -143,6 +422,7 @@ __device__ __forceinline__ void scan_role(const ScanParams& p, int w, int lane, 
     b1 = ldg_stream(codes + (seg0 + 1) * kNC + c1);
   }
   int iter = 0;
+  int prev_slot = -1;
   for (int64_t t = seg0; t < nseg; ++t, ++iter) {
     const uint4 x0 = a0, x1 = a1;
     a0 = b0;
@@ -172,7 +452,7 @@ __device__ __forceinline__ void scan_role(const ScanParams& p, int w, int lane, 
         f[v][j] = acc[0];
       }
     }
-    // items outside [k, n) never enter the prune loop (seeds / padding)
+    // items outside [start, n) never enter the replay (decided / padding)
     const int64_t base = t * S;
     if (base < p.k || base + S > p.n) {
 #pragma unroll
@@ -180,145 +460,217 @@ __device__ __forceinline__ void scan_role(const ScanParams& p, int w, int lane, 
 #pragma unroll
         for (int j = 0; j < IPC; ++j) {
           const int64_t id = base + (int64_t)(v ? c1 : c0) * IPC + j;
-          if (id < p.k || id >= p.n) f[v][j] = __int_as_float(0x7f800000);
+          if (id < p.k || id >= p.n) f[v][j] = kInf;
         }
     }
     const int slot = iter % p.nb;
     const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
-    mbar_wait(ctrl + 32 + 8 * slot, par ^ 1u);  // empty[slot]
-    const uint32_t vb = p.off_slot[slot];
-    const uint32_t gb = vb + IPC * kValStride * 4;
+    mbar_wait(c.ctrl + 32 + 8 * slot, par ^ 1u);  // empty[slot]
+    const uint32_t sb = p.off_slot[slot];
+    const uint32_t vb = sb;
+    const uint32_t gb = sb + p.so_gmin;
+    float wm = kInf, lm[2];
 #pragma unroll
     for (int v = 0; v < 2; ++v) {
-      const int c = v ? c1 : c0;
+      const int cc = v ? c1 : c0;
       float mn = f[v][0];
 #pragma unroll
       for (int j = 0; j < IPC; ++j) {
-        sts_f32(vb + (uint32_t)(j * kValStride + c) * 4, f[v][j]);
+        sts_f32(vb + (uint32_t)(j * kValStride + cc) * 4, f[v][j]);
         mn = fminf(mn, f[v][j]);
       }
-      sts_f32(gb + (uint32_t)c * 4, mn);
+      sts_f32(gb + (uint32_t)cc * 4, mn);
+      lm[v] = mn;
+      wm = fminf(wm, mn);
     }
-    mbar_arrive(ctrl + 8 * slot);  // full[slot]
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wm = fminf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    if (lane == 0) sts_f32(sb + p.so_wmin + 4 * w, wm);
+
+    // rows of likely candidates -> slot (cp.async), float64 scores next round
+    int ecnt = 0;
+    if (p.cw > 0) {
+      const float pt = *pub;
+      if (__any_sync(0xffffffffu, fminf(lm[0], lm[1]) < pt)) {
+        uint16_t* rcidx = reinterpret_cast<uint16_t*>(c.at(sb + p.so_rcidx));
+        int32_t* eid = reinterpret_cast<int32_t*>(c.at(sb + p.so_eid));
+        const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int cc = v ? c1 : c0;
+#pragma unroll
+          for (int j = 0; j < IPC; ++j) {
+            const bool hit = f[v][j] < pt;
+            const uint32_t bm = __ballot_sync(0xffffffffu, hit);
+            const int slotpos = ecnt + __popc(bm & below);
+            if (hit && slotpos < p.cw) {
+              const int e = w * p.cw + slotpos;
+              const int il = cc * IPC + j;
+              const int64_t id = base + il;
+              rcidx[il] = (uint16_t)e;
+              eid[e] = (int32_t)id;
+              cp_async_row(sb + p.so_erow + (uint32_t)e * 16, p.codes_full + id * p.KP, rowb);
+            }
+            ecnt += __popc(bm);
+          }
+        }
+        if (ecnt > p.cw) ecnt = p.cw;
+      }
+    }
+    if (lane == 0) *reinterpret_cast<volatile int32_t*>(c.at(sb + p.so_ecnt + 4 * w)) = ecnt;
+    cp_async_commit();
+    // finalize the previous segment: its rows have landed (all but the newest group)
+    if (prev_slot >= 0) {
+      cp_async_wait<1>();
+      __syncwarp();
+      scan_finalize<FP>(c, prev_slot, w, lane);
+      mbar_arrive(c.ctrl + 8 * prev_slot);  // full[prev]
+    }
+    prev_slot = slot;
+  }
+  if (prev_slot >= 0) {
+    cp_async_wait<0>();
+    __syncwarp();
+    scan_finalize<FP>(c, prev_slot, w, lane);
+    mbar_arrive(c.ctrl + 8 * prev_slot);
   }
 }
 
 // --------------------------------------------------------------------------
-// REPLAY warp
+// Phase 2, REPLAY warp
 // --------------------------------------------------------------------------
-struct ReplayState {
-  double T64, bound64, thr64;
-  float lo, hi;
-  int64_t refinements, insertions, candidates, certified;
-};
-
 template <int FP>
-__device__ __forceinline__ void replay_role(const ScanParams& p, int lane, uint32_t ctrl,
-                                            const double* lut, double* he, double* hf,
-                                            int32_t* hi, bool wide, int64_t* counters) {
+__device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int64_t seg0) {
   using G = Geo<FP>;
   constexpr int IPC = G::IPC;
   constexpr int S = G::S;
+  constexpr int GPB = 32 / IPC;  // groups per 32-lane batch
+  const ScanParams& p = *c.p;
   const int F = p.F;
-  const int K = p.K;
-  const int m = p.m;
   const int k = p.k;
   const int64_t n = p.n;
-  const bool pw = n == 1;
+  const bool wide = c.wide;
   uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
+  const int ncache = kNS * p.cw;
 
-  double T64 = he[0], bound64 = hf[0];
-  double thr64 = __dadd_rn(bound64, p.sigma);
-  float lo, hi_f;
-  certified_bounds(thr64, F, lo, hi_f);
-  if (wide) { lo = -__int_as_float(0x7f800000); hi_f = __int_as_float(0x7f800000); }
-  int64_t refinements = 0, insertions = 0, candidates = 0, certified = 0;
-
-  const int64_t seg0 = p.k / S;
   int iter = 0;
   for (int64_t t = seg0; t < p.nseg; ++t, ++iter) {
     const int slot = iter % p.nb;
     const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
-    mbar_wait(ctrl + 8 * slot, par);  // full[slot]
-    const uint32_t vb = p.off_slot[slot];
-    const uint32_t gb = vb + IPC * kValStride * 4;
+    const long long tw = clock64();
+    mbar_wait(c.ctrl + 8 * slot, par);  // full[slot]
+    L.wait_cycles += clock64() - tw;
+    const uint32_t sb = p.off_slot[slot];
+    const float* wmin = reinterpret_cast<const float*>(c.at(sb + p.so_wmin));
+    const float* gmin = reinterpret_cast<const float*>(c.at(sb + p.so_gmin));
+    const uint16_t* rcidx = reinterpret_cast<const uint16_t*>(c.at(sb + p.so_rcidx));
+    const int32_t* eid = reinterpret_cast<const int32_t*>(c.at(sb + p.so_eid));
+    const double* ef64 = reinterpret_cast<const double*>(c.at(sb + p.so_ef64));
+    const double* ee64 = reinterpret_cast<const double*>(c.at(sb + p.so_ee64));
     const int64_t base = t * S;
-    for (int r = 0; r < kNC / 32; ++r) {
-      const int cg = r * 32 + lane;
-      const float g = lds_f32(gb + (uint32_t)cg * 4);
-      const int64_t gid0 = base + (int64_t)cg * IPC;
-      const bool gvalid = gid0 + IPC > k && gid0 < n;
-      uint32_t cm = __ballot_sync(0xffffffffu, gvalid && (wide || g < hi_f));
-      while (cm) {
-        const int cl = __ffs(cm) - 1;
-        const int c = r * 32 + cl;
-        // ---- expand group c: lane j <-> item base + c*IPC + j --------------
-        const bool act = lane < IPC;
-        const int64_t id = base + (int64_t)c * IPC + lane;
-        const bool valid = act && id >= k && id < n;
-        const float fv = act ? lds_f32(vb + (uint32_t)(lane * kValStride + c) * 4) : 0.f;
+
+    const float wmv = lane < kNS ? wmin[lane] : kInf;
+    uint32_t wmask = __ballot_sync(0xffffffffu, lane < kNS && (wide || wmv < L.hi));
+    while (wmask) {
+      const int w = __ffs(wmask) - 1;
+      // this warp's 64 groups, in item order: c = w*64 + v*32 + lane
+      const float g0 = gmin[w * 64 + lane];
+      const float g1 = gmin[w * 64 + 32 + lane];
+      uint64_t gm = (uint64_t)__ballot_sync(0xffffffffu, wide || g0 < L.hi) |
+                    ((uint64_t)__ballot_sync(0xffffffffu, wide || g1 < L.hi) << 32);
+      while (gm) {
+        // batch: the next GPB candidate groups, lane <-> (group gi, item j)
+        const int gi = lane / IPC;
+        const int j = lane % IPC;
+        uint64_t tmp = gm;
+        int mygrp = -1, lastgrp = -1;
+        for (int q = 0; q < GPB && tmp; ++q) {
+          const int g = __ffsll((long long)tmp) - 1;
+          tmp &= tmp - 1;
+          if (q == gi) mygrp = g;
+          lastgrp = g;
+        }
+        const int cc = w * 64 + (mygrp < 0 ? 0 : mygrp);
+        const int il = cc * IPC + j;
+        const int64_t id = base + il;
+        const bool valid = mygrp >= 0 && id >= k && id < n;
+        const float fv = valid ? lds_f32(sb + (uint32_t)(j * kValStride + cc) * 4) : kInf;
+        // cached float64 scores (precomputed by the scan warps)
+        double cf = 0.0, ce = 0.0;
+        bool cached = false;
+        if (valid && ncache > 0) {
+          const int e = rcidx[il];
+          if (e < ncache && eid[e] == (int32_t)id) {
+            cached = true;
+            cf = ef64[e];
+            ce = ee64[e];
+          }
+        }
         uint32_t done = 0;
         for (;;) {
-          const bool cand = valid && !((done >> lane) & 1u) && (wide || fv < hi_f);
+          const bool cand = valid && !((done >> lane) & 1u) && (wide || fv < L.hi);
           const uint32_t cmask = __ballot_sync(0xffffffffu, cand);
           if (!cmask) break;
-          bool refined = false, have_row = false, have_f64 = false;
-          double f64 = 0.0, e64 = 0.0;
-          Row row;
+          bool refined = false;
+          bool certified = false;
+          double f64 = cf, e64 = ce;
           if (cand) {
-            if (!wide && fv < lo) {
+            if (!wide && fv < L.lo) {
               refined = true;
             } else {
-              row = load_row(p.codes_full, p.KP, id);
-              have_row = true;
-              f64 = fast64(lut, m, F, pw, p.fast_books, row);
-              have_f64 = true;
-              refined = f64 < thr64;
+              if (!cached) {
+                const Row r = load_row(p.codes_full, p.KP, id);
+                cf = f64 = fast64(c.lut, p.m, F, c.pw, p.fast_books, r);
+                ce = e64 = exact64(c.lut, p.m, p.K, c.pw, r);
+                cached = true;
+              }
+              certified = true;
+              refined = f64 < L.thr64;
+            }
+            if (refined && !cached) {
+              const Row r = load_row(p.codes_full, p.KP, id);
+              cf = f64 = fast64(c.lut, p.m, F, c.pw, p.fast_books, r);
+              ce = e64 = exact64(c.lut, p.m, p.K, c.pw, r);
+              cached = true;
             }
           }
-          const uint32_t cert = __ballot_sync(0xffffffffu, cand && have_f64);
-          if (refined) {
-            if (!have_row) row = load_row(p.codes_full, p.KP, id);
-            have_row = true;
-            e64 = exact64(lut, m, K, pw, row);
-          }
-          const bool ins = refined && (e64 < T64);
+          const bool ins = refined && (e64 < L.T64);
           const uint32_t rmask = __ballot_sync(0xffffffffu, refined);
           const uint32_t imask = __ballot_sync(0xffffffffu, ins);
+          const uint32_t cert = __ballot_sync(0xffffffffu, certified);
           const int first = imask ? __ffs(imask) - 1 : 31;
           const uint32_t decided = imask ? (0xffffffffu >> (31 - first)) : 0xffffffffu;
-          refinements += __popc(rmask & decided);
-          candidates += __popc(cmask & decided);
-          certified += __popc(cert & decided);
-          if (surv && refined && ((decided >> lane) & 1u))
-            atomicOr(surv + (id >> 5), 1u << (id & 31));
+          L.refinements += __popc(rmask & decided);
+          L.candidates += __popc(cmask & decided);
+          L.certified += __popc(cert & decided);
+          if (refined && ((decided >> lane) & 1u)) record_survivor(surv, id);
           done |= decided;
           if (!imask) break;
-          // ---- insertion of lane `first` (search.py:152-154) --------------
-          if (lane == first && !have_f64) f64 = fast64(lut, m, F, pw, p.fast_books, row);
+          // insertion (search.py:152-154)
           const double ne = __shfl_sync(0xffffffffu, e64, first);
           const double nf = __shfl_sync(0xffffffffu, f64, first);
           const int32_t nid = (int32_t)__shfl_sync(0xffffffffu, (int32_t)id, first);
-          heap_replace_max(he, hf, hi, k, ne, nid, nf, lane);
-          T64 = he[0];
-          bound64 = hf[0];
-          thr64 = __dadd_rn(bound64, p.sigma);
-          if (!wide) certified_bounds(thr64, F, lo, hi_f);
-          ++insertions;
+          L.H.replace_max(ne, nid, nf, lane);
+          live_update(L, c, F, p.sigma, wide, k, lane);
+          ++L.insertions;
+          // The threshold moved: groups after the inserting item's group were
+          // gated with the old one (and gated-out groups between batch members
+          // were skipped), so cut the batch here; later groups are re-gated.
+          const int gfirst = __shfl_sync(0xffffffffu, mygrp, first);
+          done |= __ballot_sync(0xffffffffu, mygrp > gfirst);
+          lastgrp = gfirst;
         }
-        // the bound may have moved: re-test the remaining groups of this round
-        const uint32_t above = (cl == 31) ? 0u : (0xffffffffu << (cl + 1));
-        cm = __ballot_sync(0xffffffffu, gvalid && (wide || g < hi_f)) & above;
+        // drop the processed groups; the bound may have moved either way, so
+        // re-test every later group of this warp against the live threshold
+        const uint64_t later = (lastgrp >= 63) ? 0ull : (~0ull << (lastgrp + 1));
+        gm = later & ((uint64_t)__ballot_sync(0xffffffffu, wide || g0 < L.hi) |
+                      ((uint64_t)__ballot_sync(0xffffffffu, wide || g1 < L.hi) << 32));
       }
+      const uint32_t later_w = (w >= 31) ? 0u : (0xffffffffu << (w + 1));
+      wmask = later_w & __ballot_sync(0xffffffffu, lane < kNS && (wide || wmv < L.hi));
     }
     __syncwarp();
-    mbar_arrive(ctrl + 32 + 8 * slot);  // empty[slot]
-  }
-  if (lane == 0) {
-    counters[0] = refinements;
-    counters[1] = insertions;
-    counters[2] = candidates;
-    counters[3] = certified;
+    mbar_arrive(c.ctrl + 32 + 8 * slot);  // empty[slot]
   }
 }
 
@@ -343,20 +695,22 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
     if (tid == 0) atomicExch(p.error, 1);
     return;
   }
-  auto sptr = [&](uint32_t abs) { return dsm + (abs - dbase); };
-  double* lut = reinterpret_cast<double*>(sptr(p.off_lut64));
-  double* he = reinterpret_cast<double*>(sptr(p.off_heap_e));
-  double* hf = reinterpret_cast<double*>(sptr(p.off_heap_f));
-  int32_t* hi = reinterpret_cast<int32_t*>(sptr(p.off_heap_i));
-  int64_t* counters = reinterpret_cast<int64_t*>(sptr(p.off_ctrl + 64));
-  const uint32_t ctrl = p.off_ctrl;
+  Ctx c;
+  c.p = &p;
+  c.dsm = dsm;
+  c.dbase = dbase;
+  c.lut = reinterpret_cast<double*>(c.at(p.off_lut64));
+  c.he = reinterpret_cast<double*>(c.at(p.off_heap_e));
+  c.hf = reinterpret_cast<double*>(c.at(p.off_heap_f));
+  c.hi = reinterpret_cast<int32_t*>(c.at(p.off_heap_i));
+  c.ctrl = p.off_ctrl;
+  c.pw = p.n == 1;  // numpy row-sum order, see ref_row_sum
 
   const int K = p.K, m = p.m, F = p.F, k = p.k;
-  const bool pw = p.n == 1;  // numpy row-sum order, see ref_row_sum
   const double* glut = p.lut64 + (size_t)q * K * m;
 
   // 1. float64 LUT -> smem; float32 lane-private replicated pages for the fast books
-  for (int i = tid; i < K * m; i += kThreads) lut[i] = glut[i];
+  for (int i = tid; i < K * m; i += kThreads) c.lut[i] = glut[i];
   bool bad = false;
   for (int i = tid; i < FP * m * G::R; i += kThreads) {
     const int s = i / (m * G::R);
@@ -375,11 +729,11 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   }
   if (tid == 0) {
     for (int s = 0; s < p.nb; ++s) {
-      mbar_init(ctrl + 8 * s, kNS * 32);   // full: every scan thread arrives
-      mbar_init(ctrl + 32 + 8 * s, 32);    // empty: every replay lane arrives
+      mbar_init(c.ctrl + 8 * s, kNS * 32);   // full: every scan thread arrives
+      mbar_init(c.ctrl + 32 + 8 * s, 32);    // empty: every replay lane arrives
     }
   }
-  const bool wide = __syncthreads_or(bad) != 0;
+  c.wide = __syncthreads_or(bad) != 0;
 
   // 2. seeds: ids 0..k-1 scored exactly (search.py:141), sorted descending
   //    by (exact, id) -> the sorted array is a valid max-heap.
@@ -391,9 +745,9 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
     const int i = tid + r * kThreads;
     if (i < k) {
       const Row row = load_row(p.codes_full, p.KP, i);
-      se[r] = exact64(lut, m, K, pw, row);
-      sf[r] = fast64(lut, m, F, pw, p.fast_books, row);
-      he[i] = se[r];
+      se[r] = exact64(c.lut, m, K, c.pw, row);
+      sf[r] = fast64(c.lut, m, F, c.pw, p.fast_books, row);
+      c.he[i] = se[r];
     }
   }
   __syncthreads();
@@ -402,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
     const int i = tid + r * kThreads;
     if (i < k) {
       int rank = 0;
-      for (int j = 0; j < k; ++j) rank += key_gt(he[j], j, se[r], i) ? 1 : 0;
+      for (int j = 0; j < k; ++j) rank += key_gt(c.he[j], j, se[r], i) ? 1 : 0;
       sr[r] = rank;
     }
   }
@@ -411,34 +765,60 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   for (int r = 0; r < kSeedPer; ++r) {
     const int i = tid + r * kThreads;
     if (i < k) {
-      he[sr[r]] = se[r];
-      hf[sr[r]] = sf[r];
-      hi[sr[r]] = i;
+      c.he[sr[r]] = se[r];
+      c.hf[sr[r]] = sf[r];
+      c.hi[sr[r]] = i;
     }
   }
   __syncthreads();
 
-  // 3. persistent scan / replay
+  Live L;
+  L.refinements = L.insertions = L.candidates = L.certified = L.wait_cycles = 0;
+  L.H.k = k;
+  L.H.reg = k <= 32 * kRegHeapRegs;
+  L.H.he = c.he;
+  L.H.hf = c.hf;
+  L.H.hi = c.hi;
   if (warp == 0) {
-    replay_role<FP>(p, lane, ctrl, lut, he, hf, hi, wide, counters);
-  } else {
-    scan_role<FP>(p, warp - 1, lane, ctrl);
+    L.H.load(lane);
+    live_update(L, c, F, p.sigma, c.wide, k, lane);
   }
   __syncthreads();
+  const long long t_setup = clock64();
 
-  // 4. output: heap ascending by (score, id) (search.py:156-165)
+  // 3. phase 1: dense prologue over the insertion-heavy start
+  const int64_t start = dense_prologue<FP>(c, L, tid, warp, lane);
+  const int64_t seg0 = (start + G::S - 1) / G::S;  // start is a segment boundary or n
+  const long long t_pro = clock64();
+
+  // 4. phase 2: pipelined scan / replay
+  if (warp == 0) {
+    replay_role<FP>(c, L, lane, seg0);
+  } else {
+    scan_role<FP>(c, warp - 1, lane, seg0);
+  }
+  const long long t_scan = clock64();
+  if (warp == 0) L.H.store(lane);
+  __syncthreads();
+
+  // 5. output: heap ascending by (score, id) (search.py:156-165)
   for (int i = tid; i < k; i += kThreads) {
     const int src = k - 1 - i;
-    p.ids[(size_t)q * k + i] = hi[src];
-    p.scores[(size_t)q * k + i] = he[src];
+    p.ids[(size_t)q * k + i] = c.hi[src];
+    p.scores[(size_t)q * k + i] = c.he[src];
   }
-  if (tid == 0) {
-    if (p.refinements) p.refinements[q] = counters[0];
+  if (warp == 0 && lane == 0) {
+    if (p.refinements) p.refinements[q] = p.exact_mode ? p.n : L.refinements;
     if (p.stats) {
-      p.stats[(size_t)q * 4 + 0] = counters[1];
-      p.stats[(size_t)q * 4 + 1] = counters[2];
-      p.stats[(size_t)q * 4 + 2] = counters[3];
-      p.stats[(size_t)q * 4 + 3] = wide ? 1 : 0;
+      int64_t* st = p.stats + (size_t)q * kStats;
+      st[0] = L.insertions;
+      st[1] = L.candidates;
+      st[2] = L.certified;
+      st[3] = start;
+      st[4] = t_pro - t_setup;       // prologue cycles
+      st[5] = t_scan - t_pro;        // phase-2 cycles (replay warp)
+      st[6] = L.wait_cycles;         // replay cycles waiting for scan warps
+      st[7] = c.wide ? 1 : 0;
     }
   }
 }
@@ -446,61 +826,88 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
 // --------------------------------------------------------------------------
 // host side: layout planning + launch
 // --------------------------------------------------------------------------
-struct ScanLayout {
-  bool ok;
-  uint32_t dyn_bytes;
-  int nb;
-};
-
 template <int FP>
-static ScanLayout plan_layout(ScanParams& p) {
+static bool plan_layout(ScanParams& p) {
   using G = Geo<FP>;
-  ScanLayout L{false, 0, 0};
   const int K = p.K, m = p.m, k = p.k;
   // regions: A = [kDynBase, 64K), pages, B = [end of used pages, window end)
   const uint32_t pages_end = kPage * G::P + (uint32_t)m * 256;
-  struct Region { uint32_t cur, end; } A{kDynBase, kPage}, B{(pages_end + 15u) & ~15u, kSmemWindow};
+  struct Region {
+    uint32_t cur, end;
+  } A{kDynBase, kPage}, B{(pages_end + 15u) & ~15u, kSmemWindow};
   auto place = [&](uint32_t bytes, uint32_t* off) {
     bytes = (bytes + 15u) & ~15u;
     if (A.cur + bytes <= A.end) { *off = A.cur; A.cur += bytes; return true; }
     if (B.cur + bytes <= B.end) { *off = B.cur; B.cur += bytes; return true; }
     return false;
   };
-  if (!place((uint32_t)K * m * 8, &p.off_lut64)) return L;
-  if (!place(128 + 64, &p.off_ctrl)) return L;
-  if (!place((uint32_t)k * 8, &p.off_heap_e)) return L;
-  if (!place((uint32_t)k * 8, &p.off_heap_f)) return L;
-  if (!place((uint32_t)k * 4, &p.off_heap_i)) return L;
-  int nb = 0;
-  for (; nb < 3; ++nb)
-    if (!place(G::slot_bytes, &p.off_slot[nb])) break;
-  if (nb < 2) return L;
-  p.nb = nb;
-  const uint32_t end = B.cur > pages_end ? B.cur : pages_end;
-  p.smem_end = end;
-  L.ok = true;
-  L.nb = nb;
-  L.dyn_bytes = end - kDynBase;
-  return L;
+  if (!place((uint32_t)K * m * 8, &p.off_lut64)) return false;
+  if (!place(kCtrlBytes, &p.off_ctrl)) return false;
+  if (!place((uint32_t)k * 8, &p.off_heap_e)) return false;
+  if (!place((uint32_t)k * 8, &p.off_heap_f)) return false;
+  if (!place((uint32_t)k * 4, &p.off_heap_i)) return false;
+  auto al16 = [](uint32_t x) { return (x + 15u) & ~15u; };
+  // slot sub-layout for a per-warp cache of `cw` rows
+  auto slot_layout = [&](int cw) {
+    uint32_t o = al16(G::IPC * kValStride * 4);
+    p.so_gmin = o;   o = al16(o + kNC * 4);
+    p.so_wmin = o;   o = al16(o + 32 * 4);
+    p.so_ecnt = o;   o = al16(o + 32 * 4);
+    p.so_rcidx = o;  o = al16(o + G::S * 2);
+    p.so_eid = o;    o = al16(o + kNS * cw * 4);
+    p.so_ef64 = o;   o = al16(o + kNS * cw * 8);
+    p.so_ee64 = o;   o = al16(o + kNS * cw * 8);
+    p.so_erow = o;   o = al16(o + kNS * cw * 16);
+    return o;
+  };
+  const int cw_pref[] = {64, 32, 16, 8, 0};
+  for (int nb = 3; nb >= 2; --nb) {
+    for (int cw : cw_pref) {
+      if (p.KP < 4 && cw) continue;  // rows narrower than a cp.async unit: no cache
+      Region a0 = A, b0 = B;
+      const uint32_t sbytes = slot_layout(cw);
+      bool ok = true;
+      for (int s = 0; s < nb && ok; ++s) ok = place(sbytes, &p.off_slot[s]);
+      if (ok) {
+        p.nb = nb;
+        p.cw = cw;
+        int C = 2048;
+        while (C > 32 && ((uint32_t)C * 16 > sbytes || C > G::S)) C >>= 1;
+        p.dense_chunk = C;
+        const uint32_t end = B.cur > pages_end ? B.cur : pages_end;
+        p.smem_end = end;
+        p.dyn_bytes = end - kDynBase;
+        return true;
+      }
+      A = a0;
+      B = b0;
+    }
+  }
+  return false;
 }
 
 template <int FP>
 static cudaError_t launch_fp(ScanParams& p, int Q, cudaStream_t s, int* unsupported) {
   using G = Geo<FP>;
   p.nseg = (p.n + G::S - 1) / G::S;
-  const ScanLayout L = plan_layout<FP>(p);
-  if (!L.ok) { *unsupported = 1; return cudaSuccess; }
+  if (!plan_layout<FP>(p)) {
+    *unsupported = 1;
+    return cudaSuccess;
+  }
   cudaError_t e = cudaFuncSetAttribute(icq_scan_kernel<FP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(kSmemWindow - kDynBase));
   if (e != cudaSuccess) return e;
-  icq_scan_kernel<FP><<<Q, kThreads, L.dyn_bytes, s>>>(p);
+  icq_scan_kernel<FP><<<Q, kThreads, p.dyn_bytes, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scan(ScanParams& p, int FP, int Q, cudaStream_t s, int* unsupported) {
   *unsupported = 0;
-  if (p.k > kThreads * 8) { *unsupported = 1; return cudaSuccess; }
+  if (p.k > kThreads * 8) {
+    *unsupported = 1;
+    return cudaSuccess;
+  }
   switch (FP) {
     case 1: return launch_fp<1>(p, Q, s, unsupported);
     case 2: return launch_fp<2>(p, Q, s, unsupported);
@@ -510,6 +917,5 @@ cudaError_t launch_scan(ScanParams& p, int FP, int Q, cudaStream_t s, int* unsup
     default: *unsupported = 1; return cudaSuccess;
   }
 }
-
 
 }  // namespace icq

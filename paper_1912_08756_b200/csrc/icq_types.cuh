@@ -34,10 +34,16 @@ struct ScanParams {
   double sigma;
   int32_t K, m, KP, F;
   int32_t k;
+  int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
   int32_t nb;                 // slots in the ring
   uint32_t off_lut64, off_heap_e, off_heap_f, off_heap_i, off_ctrl;
   uint32_t off_slot[4];
+  // sub-layout of one slot (byte offsets from the slot start)
+  uint32_t so_gmin, so_wmin, so_ecnt, so_rcidx, so_eid, so_ef64, so_ee64, so_erow;
+  int32_t cw;                 // cached candidate rows per scan warp per segment
+  int32_t dense_chunk;        // items per prologue chunk
   uint32_t smem_end;          // absolute end of the planned layout
+  uint32_t dyn_bytes;
   uint8_t fast_books[kMaxK];
 };
 

@@ -28,6 +28,12 @@ from . import _native
 from .data import DeviceError, UnsupportedError, ValidationError
 
 
+# per-query int64 diagnostics written by the scan kernel (icq_b200.h stats_dev)
+STATS_FIELDS = 8
+STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
+               "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide")
+
+
 @dataclass
 class OpCounter:
     """Addition counts for one query (search.py:22-34)."""
@@ -138,9 +144,60 @@ class DeviceIndex:
         self.K, self.m, self.d, self.n, self.F = K, m, d, n, int(fast.size)
         self._fin = weakref.finalize(self, L.icq_index_destroy, h)
 
+    @classmethod
+    def from_device(cls, books: np.ndarray, codes_dev, fast: np.ndarray, stream=None):
+        """Build from uint8 (n, K) codes already on the device (torch tensor)."""
+        import torch
+
+        L = _native.lib()
+        books = np.ascontiguousarray(books, dtype=np.float32)
+        K, m, d = books.shape
+        if codes_dev.dtype != torch.uint8 or codes_dev.dim() != 2 or codes_dev.shape[1] != K:
+            raise ValidationError("codes_dev must be a cuda uint8 tensor of shape (n, K)")
+        codes_dev = codes_dev.contiguous()
+        books_dev = torch.from_numpy(books).to(codes_dev.device)
+        fast = np.ascontiguousarray(np.asarray(fast), dtype=np.uint32).reshape(-1)
+        s = stream if stream is not None else torch.cuda.current_stream(codes_dev.device).cuda_stream
+        h = C.c_void_p()
+        st = L.icq_index_create_device(books_dev.data_ptr(), K, m, d, codes_dev.data_ptr(),
+                                       codes_dev.shape[0], fast.ctypes.data, fast.size, s,
+                                       C.byref(h))
+        if st != _native.ICQ_OK:
+            _raise(st, "icq_index_create_device")
+        self = cls.__new__(cls)
+        self._h = h
+        self.K, self.m, self.d, self.n, self.F = K, m, d, int(codes_dev.shape[0]), int(fast.size)
+        self._fin = weakref.finalize(self, L.icq_index_destroy, h)
+        return self
+
     @property
     def handle(self):
         return self._h
+
+    def search_lut_device(self, lut, k: int, sigma: float = 0.0, exact: bool = False, out=None,
+                          stats=False, stream=None):
+        """Search on a precomputed device float64 LUT (nq, K, m); torch outputs."""
+        import torch
+
+        nq = lut.shape[0]
+        dev = lut.device
+        if out is None:
+            out = {
+                "ids": torch.empty((nq, k), dtype=torch.int64, device=dev),
+                "scores": torch.empty((nq, k), dtype=torch.float64, device=dev),
+                "refinements": torch.empty((nq,), dtype=torch.int64, device=dev),
+            }
+            if stats:
+                out["stats"] = torch.empty((nq, STATS_FIELDS), dtype=torch.int64, device=dev)
+        s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+        fb = C.c_int32(0)
+        st = _native.lib().icq_search_with_lut(
+            self._h, lut.data_ptr(), nq, k, float(sigma), int(exact), out["ids"].data_ptr(),
+            out["scores"].data_ptr(), out["refinements"].data_ptr(), None,
+            out["stats"].data_ptr() if "stats" in out else None, C.byref(fb), s)
+        if st != _native.ICQ_OK:
+            _raise(st, "icq_search_with_lut")
+        return out
 
     # -- host-buffer path (used by the reference-shaped API) ------------------
     def search_host(self, Q: np.ndarray, k: int, sigma: float, exact: bool):
@@ -189,7 +246,7 @@ class DeviceIndex:
                 out["survivors"] = torch.empty((nq, (self.n + 31) // 32), dtype=torch.int32,
                                                device=dev)
             if stats:
-                out["stats"] = torch.empty((nq, 4), dtype=torch.int64, device=dev)
+                out["stats"] = torch.empty((nq, STATS_FIELDS), dtype=torch.int64, device=dev)
         need = self.workspace_bytes(nq, k)
         if workspace is None or workspace.numel() < need:
             workspace = torch.empty(need, dtype=torch.uint8, device=dev)
