@@ -99,7 +99,7 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
  *   refine_dev   : int64 [Q]     ops.refinements (search.py:160); may be NULL
  *   survivors_dev: optional uint32 bitmap [Q * ceil(n/32)] of refined ids
  *                  (instrumentation for parity tests; NULL to skip)
- *   stats_dev    : optional int64 [Q*8] diagnostics per query: heap insertions,
+ *   stats_dev    : optional int64 [Q*16] diagnostics per query: heap insertions,
  *                  items examined by the in-order replay, items certified in
  *                  float64 (near-ties of the fp32 filter), end of the dense
  *                  prologue (item id), prologue cycles, phase-2 cycles,

@@ -20,7 +20,7 @@ constexpr int kValStride = kNC + 1;  // padded row stride of the slot value tabl
 constexpr uint32_t kPage = 65536;  // lane-private LUT pages live at 64 KiB-aligned smem addresses
 constexpr uint32_t kSmemWindow = 233472;  // B200: 1 KiB reserved + 227 KiB dynamic
 constexpr uint32_t kDynBase = 1024;       // dynamic smem base when the kernel has no static smem
-constexpr int kStats = 8;                 // int64 diagnostics per query (icq_b200.h stats_dev)
+constexpr int kStats = 16;                // int64 diagnostics per query (icq_b200.h stats_dev)
 
 // --------------------------------------------------------------------------
 // shared-memory access by absolute (window) address

@@ -116,7 +116,10 @@ __device__ __forceinline__ double fast64(const double* lut, int m, int F, bool p
 
 // (exact, id) ordering of the reference heap (search.py:140: keys (-exact, -id))
 __device__ __forceinline__ bool key_gt(double e1, int32_t i1, double e2, int32_t i2) {
-  return e1 > e2 || (e1 == e2 && i1 > i2);
+  // branch-free (no short-circuit): the replay warp's hot compares must not
+  // open divergence regions
+  const bool gt = e1 > e2, eq = e1 == e2, ig = i1 > i2;
+  return gt | (eq & ig);
 }
 
 // Replace the maximum (entry 0) of a descending-sorted heap by (e, id, f).
@@ -144,9 +147,12 @@ __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, dou
 
 // The replay warp's view of the heap: the k best (exact, id) entries sorted
 // descending (entry 0 = heap maximum, search.py:140).  For k <= 128 the
-// entries live in warp-0 registers (entry i = r*32 + lane) so an insertion is
-// a handful of ballots and shuffles; larger k falls back to shared memory.
+// entries live in warp-0 registers in a BLOCKED layout (lane l holds entries
+// 4l..4l+3): an insertion shifts registers locally, moves only the lane
+// boundary entry with one shuffle per field, and finds its position with one
+// __reduce_add_sync.  Larger k falls back to shared memory.
 constexpr int kRegHeapRegs = 4;
+constexpr int kTopC = 2;  // larger caches push the replay state out of registers
 struct WarpHeap {
   int k;
   bool reg;
@@ -157,68 +163,107 @@ struct WarpHeap {
   int32_t* hi;
 
   __device__ __forceinline__ void load(int lane) {
-    if (!reg) return;
+    if (reg) {
 #pragma unroll
-    for (int r = 0; r < kRegHeapRegs; ++r) {
-      const int i = r * 32 + lane;
-      e[r] = i < k ? he[i] : 0.0;
-      f[r] = i < k ? hf[i] : 0.0;
-      id[r] = i < k ? hi[i] : 0;
+      for (int r = 0; r < kRegHeapRegs; ++r) {
+        const int i = kRegHeapRegs * lane + r;
+        e[r] = i < k ? he[i] : 0.0;
+        f[r] = i < k ? hf[i] : 0.0;
+        id[r] = i < k ? hi[i] : 0;
+      }
     }
+    refill();
   }
   __device__ __forceinline__ void store(int lane) {
     if (!reg) return;
 #pragma unroll
     for (int r = 0; r < kRegHeapRegs; ++r) {
-      const int i = r * 32 + lane;
+      const int i = kRegHeapRegs * lane + r;
       if (i < k) { he[i] = e[r]; hf[i] = f[r]; hi[i] = id[r]; }
     }
     __syncwarp();
   }
-  __device__ __forceinline__ double top_e() const {
-    return reg ? __shfl_sync(0xffffffffu, e[0], 0) : he[0];
-  }
-  __device__ __forceinline__ double top_f() const {
-    return reg ? __shfl_sync(0xffffffffu, f[0], 0) : hf[0];
-  }
-  // max fast score over entries 0..R (R < 32)
-  __device__ __forceinline__ double top_fast_max(int R, int lane) const {
-    double a = (lane <= R && lane < k) ? (reg ? f[0] : hf[lane]) : 0.0;
+  // Warp-uniform copy of the top uc (<= kTopC) entries: every lane holds the
+  // same values, so the new maximum after an insertion (the reference's T and
+  // bound) is plain per-lane ALU work — no shuffle on the critical path.
+  double ue[kTopC], uf[kTopC];
+  int32_t ui[kTopC];
+  int uc;
+
+  __device__ __forceinline__ void refill() {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    for (int j = 0; j < kTopC; ++j) {
+      if (reg) {  // entries 0..kTopC-1 sit in lane 0 (kTopC <= kRegHeapRegs)
+        ue[j] = __shfl_sync(0xffffffffu, e[j], 0);
+        uf[j] = __shfl_sync(0xffffffffu, f[j], 0);
+        ui[j] = __shfl_sync(0xffffffffu, id[j], 0);
+      } else {
+        ue[j] = j < k ? he[j] : 0.0;
+        uf[j] = j < k ? hf[j] : 0.0;
+        ui[j] = j < k ? hi[j] : 0;
+      }
+    }
+    uc = k < kTopC ? k : kTopC;
+  }
+  __device__ __forceinline__ double top_e() const { return ue[0]; }
+  __device__ __forceinline__ double top_f() const { return uf[0]; }
+  // max fast score over entries 0..R
+  __device__ __forceinline__ double top_fast_max(int R, int /*lane*/) const {
+    double a = uf[0];
+#pragma unroll
+    for (int j = 1; j < kTopC; ++j)
+      if (j <= R && j < uc) a = fmax(a, uf[j]);
     return a;
   }
   __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
+    // 1. uniform top cache: drop entry 0, insert x if it ranks inside the prefix
+    double le = ue[0];  // smallest cached entry (static indexing keeps it in registers)
+    int32_t li = ui[0];
+#pragma unroll
+    for (int j = 1; j < kTopC; ++j)
+      if (j == uc - 1) { le = ue[j]; li = ui[j]; }
+    const bool in = uc >= 2 && key_gt(xe, xid, le, li);
+    // in place, top down: slot j takes old[j+1] while that still outranks x,
+    // then x, then keeps old[j]
+#pragma unroll
+    for (int j = 0; j < kTopC; ++j) {
+      const int jn = j + 1 < kTopC ? j + 1 : j;
+      const bool above_gt = (j + 1 < uc) && key_gt(ue[jn], ui[jn], xe, xid);
+      const bool here_gt = j == 0 ? true : ((j < uc) && key_gt(ue[j], ui[j], xe, xid));
+      if (above_gt) { ue[j] = ue[jn]; uf[j] = uf[jn]; ui[j] = ui[jn]; }
+      else if (here_gt && in) { ue[j] = xe; uf[j] = xf; ui[j] = xid; }
+    }
+    if (!in) --uc;
+    // 2. the full sorted array (lanes or shared memory), off the critical path
+    replace_max_array(xe, xid, xf, lane);
+    if (uc < 2 && k >= 2) refill();
+    if (k == 1) { ue[0] = xe; uf[0] = xf; ui[0] = xid; uc = 1; }
+  }
+  __device__ __forceinline__ void replace_max_array(double xe, int32_t xid, double xf, int lane) {
     if (!reg) {
       heap_replace_max(he, hf, hi, k, xe, xid, xf, lane);
       return;
     }
-    int g = 0;  // entries 1..k-1 that stay above x
+    int cnt = 0;  // this lane's entries among 1..k-1 that stay above x
 #pragma unroll
     for (int r = 0; r < kRegHeapRegs; ++r) {
-      const int i = r * 32 + lane;
-      g += __popc(__ballot_sync(0xffffffffu, i >= 1 && i < k && key_gt(e[r], id[r], xe, xid)));
+      const int i = kRegHeapRegs * lane + r;
+      cnt += ((i >= 1) & (i < k) & key_gt(e[r], id[r], xe, xid)) ? 1 : 0;
     }
-    // new[i] = old[i+1] for i < g, x at g, unchanged above
-    double se[kRegHeapRegs], sf[kRegHeapRegs];
-    int32_t si[kRegHeapRegs];
+    const int g = __reduce_add_sync(0xffffffffu, cnt);  // sorted: they are entries 1..g
+    // new[i] = old[i+1] for i < g, x at g, unchanged above; old[i+1] of the
+    // lane's last register is the next lane's first
+    const double ne = __shfl_down_sync(0xffffffffu, e[0], 1);
+    const double nf = __shfl_down_sync(0xffffffffu, f[0], 1);
+    const int32_t ni = __shfl_down_sync(0xffffffffu, id[0], 1);
 #pragma unroll
     for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = kRegHeapRegs * lane + r;
       const int rn = r + 1 < kRegHeapRegs ? r + 1 : r;
-      const double de = __shfl_down_sync(0xffffffffu, e[r], 1);
-      const double df = __shfl_down_sync(0xffffffffu, f[r], 1);
-      const int32_t di = __shfl_down_sync(0xffffffffu, id[r], 1);
-      const double ne = __shfl_sync(0xffffffffu, e[rn], 0);
-      const double nf = __shfl_sync(0xffffffffu, f[rn], 0);
-      const int32_t ni = __shfl_sync(0xffffffffu, id[rn], 0);
-      se[r] = lane == 31 ? ne : de;
-      sf[r] = lane == 31 ? nf : df;
-      si[r] = lane == 31 ? ni : di;
-    }
-#pragma unroll
-    for (int r = 0; r < kRegHeapRegs; ++r) {
-      const int i = r * 32 + lane;
-      if (i < g) { e[r] = se[r]; f[r] = sf[r]; id[r] = si[r]; }
+      const double se = r + 1 < kRegHeapRegs ? e[rn] : ne;
+      const double sf = r + 1 < kRegHeapRegs ? f[rn] : nf;
+      const int32_t si = r + 1 < kRegHeapRegs ? id[rn] : ni;
+      if (i < g) { e[r] = se; f[r] = sf; id[r] = si; }
       else if (i == g) { e[r] = xe; f[r] = xf; id[r] = xid; }
     }
   }
@@ -266,23 +311,34 @@ struct Live {
   float lo, hi;
   int64_t refinements, insertions, candidates, certified;
   int64_t wait_cycles;  // replay time spent waiting for the scan warps
+  int64_t t_score, t_decide, t_insert;  // prologue breakdown (warp 0 clocks)
   WarpHeap H;
 };
 
-__device__ __forceinline__ void live_update(Live& L, const Ctx& c, int F, double sigma, bool wide,
-                                           int k, int lane) {
+// float64 state after a heap change (all the prologue needs)
+__device__ __forceinline__ void live_update64(Live& L, double sigma) {
   L.T64 = L.H.top_e();
   L.bound64 = L.H.top_f();
   L.thr64 = __dadd_rn(L.bound64, sigma);
+}
+
+// + certified float32 thresholds for the phase-2 filter
+__device__ __forceinline__ void live_update(Live& L, const Ctx& c, int F, double sigma, bool wide,
+                                           int k, int lane) {
+  live_update64(L, sigma);
   if (wide) {
     L.lo = -kInf;
     L.hi = kInf;
   } else {
     certified_bounds(L.thr64, F, L.lo, L.hi);
   }
-  // publish the scan warps' row-prefetch threshold: the bound stays <= the
-  // max fast score over the top kPubR+1 heap entries (+ sigma per insertion)
-  // for the next kPubR insertions.
+}
+
+// Publish the scan warps' row-prefetch threshold: the bound stays <= the max
+// fast score over the top kPubR+1 heap entries (+ sigma per insertion) for
+// the next kPubR insertions.  Only steers prefetching, never correctness.
+__device__ __forceinline__ void publish_prefetch(const Live& L, const Ctx& c, int F, double sigma,
+                                                 bool wide, int lane) {
   const double a = L.H.top_fast_max(kPubR, lane);
   float lo2, hi2;
   certified_bounds(__dadd_rn(a, sigma * (kPubR + 1)), F, lo2, hi2);
@@ -300,7 +356,8 @@ __device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {
 // Phase 1: dense prologue (all warps score, warp 0 decides in float64)
 // --------------------------------------------------------------------------
 template <int FP>
-__device__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp, int lane) {
+__device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp,
+                                                  int lane) {
   using G = Geo<FP>;
   const ScanParams& p = *c.p;
   const int64_t n = p.n;
@@ -315,6 +372,7 @@ __device__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp, int 
   while (pos < n) {
     const int64_t end = min(n, (pos / C + 1) * C);
     const int cnt = (int)(end - pos);
+    const long long tc0 = clock64();
     for (int i0 = 0; i0 < cnt; i0 += kThreads * 8) {
       Row rows[8];  // issue all row loads first, then score (one memory latency per round)
 #pragma unroll
@@ -332,8 +390,20 @@ __device__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp, int 
       }
     }
     __syncthreads();
+    const long long tc1 = clock64();
+    L.t_score += tc1 - tc0;
     if (warp == 0) {
       for (int b0 = 0; b0 < cnt; b0 += 32) {
+        // no refinement in the next 128 items -> skip them (4 independent loads)
+        if (b0 + 128 <= cnt) {
+          bool any = false;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) any |= df[b0 + u * 32 + lane] < L.thr64;
+          if (!__any_sync(0xffffffffu, any)) {
+            b0 += 96;
+            continue;
+          }
+        }
         const int i = b0 + lane;
         const bool valid = i < cnt;
         const double f = valid ? df[i] : 0.0;
@@ -354,12 +424,17 @@ __device__ int64_t dense_prologue(const Ctx& c, Live& L, int tid, int warp, int 
           if (!imask) break;
           const double ne = __shfl_sync(0xffffffffu, e, first);
           const double nf = __shfl_sync(0xffffffffu, f, first);
+          const long long ti0 = clock64();
           L.H.replace_max(ne, (int32_t)(pos + b0 + first), nf, lane);
-          live_update(L, c, p.F, p.sigma, c.wide, k, lane);
+          live_update64(L, p.sigma);
+          L.t_insert += clock64() - ti0;
           ++L.insertions;
           ++seg_ins;
         }
       }
+      L.t_decide += clock64() - tc1;
+      live_update(L, c, p.F, p.sigma, c.wide, k, lane);
+      publish_prefetch(L, c, p.F, p.sigma, c.wide, lane);
       // stop at a segment boundary once the insertion rate has dropped
       bool more = end < n;
       if (end % G::S == 0) {
@@ -582,28 +657,32 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
         // batch: the next GPB candidate groups, lane <-> (group gi, item j)
         const int gi = lane / IPC;
         const int j = lane % IPC;
-        uint64_t tmp = gm;
-        int mygrp = -1, lastgrp = -1;
-        for (int q = 0; q < GPB && tmp; ++q) {
-          const int g = __ffsll((long long)tmp) - 1;
-          tmp &= tmp - 1;
-          if (q == gi) mygrp = g;
-          lastgrp = g;
-        }
+        const uint32_t lo32 = (uint32_t)gm, hi32 = (uint32_t)(gm >> 32);
+        const int nlo = __popc(lo32);
+        const int ngrp = min(GPB, nlo + __popc(hi32));
+        auto nth = [&](int q) {  // q-th set bit of gm (q < popc(gm))
+          return q < nlo ? (int)__fns(lo32, 0, q + 1) : 32 + (int)__fns(hi32, 0, q - nlo + 1);
+        };
+        int mygrp = gi < ngrp ? nth(gi) : -1;
+        int lastgrp = nth(ngrp - 1);
         const int cc = w * 64 + (mygrp < 0 ? 0 : mygrp);
         const int il = cc * IPC + j;
         const int64_t id = base + il;
         const bool valid = mygrp >= 0 && id >= k && id < n;
+        // fast score and the cache entry index are independent loads
         const float fv = valid ? lds_f32(sb + (uint32_t)(j * kValStride + cc) * 4) : kInf;
-        // cached float64 scores (precomputed by the scan warps)
+        const int e = (valid && ncache > 0) ? (int)rcidx[il] : ncache;
+        // cached float64 scores (precomputed by the scan warps); loaded
+        // speculatively next to the id check
         double cf = 0.0, ce = 0.0;
         bool cached = false;
-        if (valid && ncache > 0) {
-          const int e = rcidx[il];
-          if (e < ncache && eid[e] == (int32_t)id) {
+        if (e < ncache) {
+          const int32_t eidv = eid[e];
+          const double cfv = ef64[e], cev = ee64[e];
+          if (eidv == (int32_t)id) {
             cached = true;
-            cf = ef64[e];
-            ce = ee64[e];
+            cf = cfv;
+            ce = cev;
           }
         }
         uint32_t done = 0;
@@ -671,6 +750,7 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
     }
     __syncwarp();
     mbar_arrive(c.ctrl + 32 + 8 * slot);  // empty[slot]
+    publish_prefetch(L, c, F, p.sigma, wide, lane);
   }
 }
 
@@ -774,6 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
 
   Live L;
   L.refinements = L.insertions = L.candidates = L.certified = L.wait_cycles = 0;
+  L.t_score = L.t_decide = L.t_insert = 0;
   L.H.k = k;
   L.H.reg = k <= 32 * kRegHeapRegs;
   L.H.he = c.he;
@@ -782,6 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   if (warp == 0) {
     L.H.load(lane);
     live_update(L, c, F, p.sigma, c.wide, k, lane);
+    publish_prefetch(L, c, F, p.sigma, c.wide, lane);
   }
   __syncthreads();
   const long long t_setup = clock64();
@@ -819,6 +901,9 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
       st[5] = t_scan - t_pro;        // phase-2 cycles (replay warp)
       st[6] = L.wait_cycles;         // replay cycles waiting for scan warps
       st[7] = c.wide ? 1 : 0;
+      st[8] = L.t_score;
+      st[9] = L.t_decide;
+      st[10] = L.t_insert;
     }
   }
 }

@@ -29,9 +29,11 @@ from .data import DeviceError, UnsupportedError, ValidationError
 
 
 # per-query int64 diagnostics written by the scan kernel (icq_b200.h stats_dev)
-STATS_FIELDS = 8
+STATS_FIELDS = 16
 STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
-               "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide")
+               "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide",
+               "prologue_score_cycles", "prologue_decide_cycles", "prologue_insert_cycles",
+               "r11", "r12", "r13", "r14", "r15")
 
 
 @dataclass
