@@ -80,8 +80,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
 template <typename TermFn>
 __device__ __forceinline__ double ref_row_sum(int nterms, bool pairwise, TermFn t) {
   if (!pairwise || nterms < 8) {
+    // issue every table load first (nterms <= kMaxK), then the dependent adds
+    double v[kMaxK];
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i) v[i] = i < nterms ? t(i) : 0.0;
     double r = 0.0;
-    for (int i = 0; i < nterms; ++i) r = __dadd_rn(r, t(i));
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+      if (i < nterms) r = __dadd_rn(r, v[i]);
     return r;
   }
   double r0 = t(0), r1 = t(1), r2 = t(2), r3 = t(3), r4 = t(4), r5 = t(5), r6 = t(6), r7 = t(7);

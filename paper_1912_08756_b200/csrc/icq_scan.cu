@@ -24,19 +24,20 @@
 //                     of register prefetch), gather |F| float32 entries per item
 //                     from lane-private replicated LUT pages (conflict-free:
 //                     entry j of book s for lane l sits in bank l; its address
-//                     is ONE byte_perm of the code word), publish per-item fast
-//                     scores and per-group / per-warp minima into a ring of
-//                     segment slots, and for items under the replay's published
-//                     prefetch threshold fetch the full code row (cp.async) and
-//                     precompute the float64 fast and exact scores one segment
-//                     later — so the order-independent work never waits.
+//                     is ONE byte_perm of the code word), publish per-group and
+//                     per-warp minima, and compact the items under the replay's
+//                     published threshold into an ordered per-warp candidate
+//                     list whose full code rows arrive by cp.async; their
+//                     float64 fast/exact scores are computed one segment later,
+//                     so the order-independent work never waits on memory.
 //   warp 0     REPLAY consumes slots strictly in database order against the
-//                     LIVE bound: warps/groups whose minimum clears the bound
-//                     are expanded 32 items at a time, candidates are decided
-//                     with certified float32 thresholds (float64 only for
-//                     near-ties), insertions update a sorted heap in shared
-//                     memory.  Everything it compares is float64 and bitwise
-//                     the reference's.
+//                     LIVE bound: the candidate lists of a segment are decided
+//                     32 at a time with certified float32 thresholds (float64
+//                     only for near-ties); if an insertion lifts the bound
+//                     above the threshold a list was filtered with, the rest of
+//                     that segment is re-derived from the codes (exact, rare).
+//                     Insertions update a register heap.  Everything compared
+//                     is float64 and bitwise the reference's.
 //   Slots are handed over with mbarriers (full: 256 scan-thread arrivals
 //   after the cp.async rows landed; empty: 32 replay-lane arrivals).
 #include "icq_types.cuh"
@@ -49,10 +50,12 @@ struct Geo {
   static constexpr int BPR = 64 / R;                             // book slots per 256-B row
   static constexpr int P = (FP + BPR - 1) / BPR;                 // 64 KiB pages
   static constexpr int IPC = 16 / FP;                            // items per 16-B chunk
-  static constexpr int S = kNC * IPC;                            // items per segment
+  static constexpr int V = FP >= 4 ? 4 : 2;                      // chunks per lane per segment
+  static constexpr int NC = kNS * 32 * V;                        // groups (chunks) per segment
+  static constexpr int S = NC * IPC;                             // items per segment
 };
 
-constexpr int kPubR = 3;             // prefetch threshold covers the next kPubR insertions
+constexpr int kPubR = 1;             // prefetch threshold covers the next kPubR insertions
 constexpr int kDenseStopIns = 6;     // leave the prologue once a segment sees <= this many
 #define kInf (__int_as_float(0x7f800000))
 
@@ -122,14 +125,14 @@ __device__ __forceinline__ bool key_gt(double e1, int32_t i1, double e2, int32_t
   return gt | (eq & ig);
 }
 
-// Replace the maximum (entry 0) of a descending-sorted heap by (e, id, f).
+// Replace the maximum (entry 0) of a descending-sorted heap in shared memory.
 __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, double e, int32_t id,
                                  double f, int lane) {
   int g = 0;
 #pragma unroll 4
   for (int base = 1; base < k; base += 32) {
     const int i = base + lane;
-    const bool gt = i < k && key_gt(he[i], hi[i], e, id);
+    const bool gt = (i < k) && key_gt(he[i < k ? i : 0], hi[i < k ? i : 0], e, id);
     g += __popc(__ballot_sync(0xffffffffu, gt));
   }
   for (int base = 0; base < g; base += 32) {
@@ -150,7 +153,9 @@ __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, dou
 // entries live in warp-0 registers in a BLOCKED layout (lane l holds entries
 // 4l..4l+3): an insertion shifts registers locally, moves only the lane
 // boundary entry with one shuffle per field, and finds its position with one
-// __reduce_add_sync.  Larger k falls back to shared memory.
+// __reduce_add_sync.  Larger k falls back to shared memory.  A warp-uniform
+// copy of the top two entries gives the new maximum (T and bound) after an
+// insertion with plain per-lane ALU work.
 constexpr int kRegHeapRegs = 4;
 constexpr int kTopC = 2;  // larger caches push the replay state out of registers
 struct WarpHeap {
@@ -161,6 +166,9 @@ struct WarpHeap {
   double* he;
   double* hf;
   int32_t* hi;
+  double ue[kTopC], uf[kTopC];
+  int32_t ui[kTopC];
+  int uc;
 
   __device__ __forceinline__ void load(int lane) {
     if (reg) {
@@ -183,13 +191,6 @@ struct WarpHeap {
     }
     __syncwarp();
   }
-  // Warp-uniform copy of the top uc (<= kTopC) entries: every lane holds the
-  // same values, so the new maximum after an insertion (the reference's T and
-  // bound) is plain per-lane ALU work — no shuffle on the critical path.
-  double ue[kTopC], uf[kTopC];
-  int32_t ui[kTopC];
-  int uc;
-
   __device__ __forceinline__ void refill() {
 #pragma unroll
     for (int j = 0; j < kTopC; ++j) {
@@ -208,7 +209,7 @@ struct WarpHeap {
   __device__ __forceinline__ double top_e() const { return ue[0]; }
   __device__ __forceinline__ double top_f() const { return uf[0]; }
   // max fast score over entries 0..R
-  __device__ __forceinline__ double top_fast_max(int R, int /*lane*/) const {
+  __device__ __forceinline__ double top_fast_max(int R) const {
     double a = uf[0];
 #pragma unroll
     for (int j = 1; j < kTopC; ++j)
@@ -301,9 +302,10 @@ struct Ctx {
   __device__ __forceinline__ uint8_t* at(uint32_t abs) const { return dsm + (abs - dbase); }
 };
 
-// ctrl block: [0,32) full[4]  [32,64) empty[4]  [64,96) counters  96 pub_thr
-//             100 prologue flag  104 int64 phase-2 start item
+// ctrl block: [0,32) full[4]  [32,64) empty[4]  96 pub_thr  100 prologue flag
 constexpr uint32_t kCtrlBytes = 128;
+// slot meta block: cnt[8] int32, pub[8] float, wmin[8] float
+constexpr uint32_t kMetaBytes = 128;
 
 // Replay state (warp 0 only; warp-uniform registers)
 struct Live {
@@ -312,6 +314,7 @@ struct Live {
   int64_t refinements, insertions, candidates, certified;
   int64_t wait_cycles;  // replay time spent waiting for the scan warps
   int64_t t_score, t_decide, t_insert;  // prologue breakdown (warp 0 clocks)
+  int64_t fallback_segments;            // segments re-derived from the codes
   WarpHeap H;
 };
 
@@ -323,8 +326,7 @@ __device__ __forceinline__ void live_update64(Live& L, double sigma) {
 }
 
 // + certified float32 thresholds for the phase-2 filter
-__device__ __forceinline__ void live_update(Live& L, const Ctx& c, int F, double sigma, bool wide,
-                                           int k, int lane) {
+__device__ __forceinline__ void live_update(Live& L, int F, double sigma, bool wide) {
   live_update64(L, sigma);
   if (wide) {
     L.lo = -kInf;
@@ -334,17 +336,17 @@ __device__ __forceinline__ void live_update(Live& L, const Ctx& c, int F, double
   }
 }
 
-// Publish the scan warps' row-prefetch threshold: the bound stays <= the max
-// fast score over the top kPubR+1 heap entries (+ sigma per insertion) for
-// the next kPubR insertions.  Only steers prefetching, never correctness.
+// Publish the scan warps' candidate-list threshold: the bound stays <= the
+// max fast score over the top kPubR+1 heap entries (+ sigma per insertion)
+// for the next kPubR insertions, so lists filtered with it stay complete.
 __device__ __forceinline__ void publish_prefetch(const Live& L, const Ctx& c, int F, double sigma,
                                                  bool wide, int lane) {
-  const double a = L.H.top_fast_max(kPubR, lane);
+  const double a = L.H.top_fast_max(kPubR);
   float lo2, hi2;
   certified_bounds(__dadd_rn(a, sigma * (kPubR + 1)), F, lo2, hi2);
   if (lane == 0) {
     volatile float* pub = reinterpret_cast<volatile float*>(c.at(c.ctrl + 96));
-    *pub = wide ? kInf : hi2;
+    *pub = wide ? kInf : fmaxf(hi2, L.hi);
   }
 }
 
@@ -433,7 +435,7 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
         }
       }
       L.t_decide += clock64() - tc1;
-      live_update(L, c, p.F, p.sigma, c.wide, k, lane);
+      live_update(L, p.F, p.sigma, c.wide);
       publish_prefetch(L, c, p.F, p.sigma, c.wide, lane);
       // stop at a segment boundary once the insertion rate has dropped
       bool more = end < n;
@@ -458,13 +460,15 @@ template <int FP>
 __device__ __forceinline__ void scan_finalize(const Ctx& c, int slot, int w, int lane) {
   const ScanParams& p = *c.p;
   const uint32_t sb = p.off_slot[slot];
-  const int cnt = *reinterpret_cast<volatile int32_t*>(c.at(sb + p.so_ecnt + 4 * w));
+  const int total = reinterpret_cast<const volatile int32_t*>(c.at(sb))[w];
+  const int cnt = total < p.cw ? total : p.cw;
   const int e0 = w * p.cw;
+  double* ef64 = reinterpret_cast<double*>(c.at(sb + p.so_ef64));
+  double* ee64 = reinterpret_cast<double*>(c.at(sb + p.so_ee64));
   for (int e = lane; e < cnt; e += 32) {
     const Row r = smem_row(c.at(sb + p.so_erow + (uint32_t)(e0 + e) * 16), p.KP);
-    reinterpret_cast<double*>(c.at(sb + p.so_ef64))[e0 + e] =
-        fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
-    reinterpret_cast<double*>(c.at(sb + p.so_ee64))[e0 + e] = exact64(c.lut, p.m, p.K, c.pw, r);
+    ef64[e0 + e] = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
+    ee64[e0 + e] = exact64(c.lut, p.m, p.K, c.pw, r);
   }
 }
 
@@ -472,6 +476,7 @@ template <int FP>
 __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t seg0) {
   using G = Geo<FP>;
   constexpr int IPC = G::IPC;
+  constexpr int V = G::V;
   constexpr int S = G::S;
   const ScanParams& p = *c.p;
   uint32_t L[FP];
@@ -481,36 +486,35 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
            (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
 
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
-  const int c0 = w * 64 + lane;  // chunk (group) ids owned by this lane
-  const int c1 = c0 + 32;
+  const int cbase = w * 32 * V + lane;  // chunk (group) v of this lane: cbase + 32 v
   const int64_t nseg = p.nseg;
   const int rowb = p.KP < 4 ? 4 : p.KP;
   const volatile float* pub = reinterpret_cast<const volatile float*>(c.at(c.ctrl + 96));
 
-  uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0, b0 = a0, b1 = a0;
-  if (seg0 < nseg) {
-    a0 = ldg_stream(codes + seg0 * kNC + c0);
-    a1 = ldg_stream(codes + seg0 * kNC + c1);
-  }
-  if (seg0 + 1 < nseg) {
-    b0 = ldg_stream(codes + (seg0 + 1) * kNC + c0);
-    b1 = ldg_stream(codes + (seg0 + 1) * kNC + c1);
+  uint4 a[V], b[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    a[v] = seg0 < nseg ? ldg_stream(codes + seg0 * G::NC + cbase + 32 * v) : make_uint4(0, 0, 0, 0);
+    b[v] = seg0 + 1 < nseg ? ldg_stream(codes + (seg0 + 1) * G::NC + cbase + 32 * v)
+                           : make_uint4(0, 0, 0, 0);
   }
   int iter = 0;
   int prev_slot = -1;
   for (int64_t t = seg0; t < nseg; ++t, ++iter) {
-    const uint4 x0 = a0, x1 = a1;
-    a0 = b0;
-    a1 = b1;
-    if (t + 2 < nseg) {
-      b0 = ldg_stream(codes + (t + 2) * kNC + c0);
-      b1 = ldg_stream(codes + (t + 2) * kNC + c1);
-    }
-    float f[2][IPC];
+    uint4 x[V];
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const uint4 x = v ? x1 : x0;
-      const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+    for (int v = 0; v < V; ++v) {
+      x[v] = a[v];
+      a[v] = b[v];
+    }
+    if (t + 2 < nseg) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) b[v] = ldg_stream(codes + (t + 2) * G::NC + cbase + 32 * v);
+    }
+    float f[V][IPC];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
 #pragma unroll
       for (int j = 0; j < IPC; ++j) {
         float acc[FP];
@@ -527,72 +531,77 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
         f[v][j] = acc[0];
       }
     }
-    // items outside [start, n) never enter the replay (decided / padding)
     const int64_t base = t * S;
-    if (base < p.k || base + S > p.n) {
+    if (base + S > p.n) {  // padding past n never enters the replay
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
+      for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int j = 0; j < IPC; ++j) {
-          const int64_t id = base + (int64_t)(v ? c1 : c0) * IPC + j;
-          if (id < p.k || id >= p.n) f[v][j] = kInf;
-        }
+        for (int j = 0; j < IPC; ++j)
+          if (base + (int64_t)(cbase + 32 * v) * IPC + j >= p.n) f[v][j] = kInf;
     }
+    float gm[V];
+    float lm = kInf;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      gm[v] = f[v][0];
+#pragma unroll
+      for (int j = 1; j < IPC; ++j) gm[v] = fminf(gm[v], f[v][j]);
+      lm = fminf(lm, gm[v]);
+    }
+    // non-negative floats order like their bit patterns: one redux for the warp min
+    const float wm = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(lm)));
+
     const int slot = iter % p.nb;
     const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
     mbar_wait(c.ctrl + 32 + 8 * slot, par ^ 1u);  // empty[slot]
     const uint32_t sb = p.off_slot[slot];
-    const uint32_t vb = sb;
-    const uint32_t gb = sb + p.so_gmin;
-    float wm = kInf, lm[2];
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int cc = v ? c1 : c0;
-      float mn = f[v][0];
-#pragma unroll
-      for (int j = 0; j < IPC; ++j) {
-        sts_f32(vb + (uint32_t)(j * kValStride + cc) * 4, f[v][j]);
-        mn = fminf(mn, f[v][j]);
-      }
-      sts_f32(gb + (uint32_t)cc * 4, mn);
-      lm[v] = mn;
-      wm = fminf(wm, mn);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) wm = fminf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-    if (lane == 0) sts_f32(sb + p.so_wmin + 4 * w, wm);
+    for (int v = 0; v < V; ++v) sts_f32(sb + p.so_gmin + (uint32_t)(cbase + 32 * v) * 4, gm[v]);
 
-    // rows of likely candidates -> slot (cp.async), float64 scores next round
-    int ecnt = 0;
-    if (p.cw > 0) {
-      const float pt = *pub;
-      if (__any_sync(0xffffffffu, fminf(lm[0], lm[1]) < pt)) {
-        uint16_t* rcidx = reinterpret_cast<uint16_t*>(c.at(sb + p.so_rcidx));
-        int32_t* eid = reinterpret_cast<int32_t*>(c.at(sb + p.so_eid));
-        const uint32_t below = (1u << lane) - 1u;
+    // ordered candidate list: items with f < pub, in item order (v, lane, j)
+    const float pt = *pub;
+    int total = 0;
+    if (__any_sync(0xffffffffu, lm < pt)) {
+      int32_t* eid = reinterpret_cast<int32_t*>(c.at(sb + p.so_eid));
+      float* ef32 = reinterpret_cast<float*>(c.at(sb + p.so_ef32));
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int cc = v ? c1 : c0;
+      for (int v = 0; v < V; ++v) {
+        uint32_t mask = 0;
 #pragma unroll
-          for (int j = 0; j < IPC; ++j) {
-            const bool hit = f[v][j] < pt;
-            const uint32_t bm = __ballot_sync(0xffffffffu, hit);
-            const int slotpos = ecnt + __popc(bm & below);
-            if (hit && slotpos < p.cw) {
-              const int e = w * p.cw + slotpos;
-              const int il = cc * IPC + j;
-              const int64_t id = base + il;
-              rcidx[il] = (uint16_t)e;
-              eid[e] = (int32_t)id;
-              cp_async_row(sb + p.so_erow + (uint32_t)e * 16, p.codes_full + id * p.KP, rowb);
-            }
-            ecnt += __popc(bm);
-          }
+        for (int j = 0; j < IPC; ++j) mask |= (f[v][j] < pt ? 1u : 0u) << j;
+        const int my = __popc(mask);
+        int incl = my;  // inclusive scan over lanes
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
-        if (ecnt > p.cw) ecnt = p.cw;
+        int pos = total + incl - my;
+        total += __shfl_sync(0xffffffffu, incl, 31);
+        while (mask) {
+          const int j = __ffs(mask) - 1;
+          mask &= mask - 1;
+          if (pos < p.cw) {
+            const int e = w * p.cw + pos;
+            const int64_t id = base + (int64_t)(cbase + 32 * v) * IPC + j;
+            eid[e] = (int32_t)id;
+            float fj = f[v][0];
+#pragma unroll
+            for (int jj = 1; jj < IPC; ++jj)
+              if (jj == j) fj = f[v][jj];
+            ef32[e] = fj;
+            cp_async_row(sb + p.so_erow + (uint32_t)e * 16, p.codes_full + id * p.KP, rowb);
+          }
+          ++pos;
+        }
       }
     }
-    if (lane == 0) *reinterpret_cast<volatile int32_t*>(c.at(sb + p.so_ecnt + 4 * w)) = ecnt;
+    if (lane == 0) {
+      volatile int32_t* meta = reinterpret_cast<volatile int32_t*>(c.at(sb));
+      meta[w] = total;
+      reinterpret_cast<volatile float*>(meta)[8 + w] = pt;
+      reinterpret_cast<volatile float*>(meta)[16 + w] = wm;
+    }
     cp_async_commit();
     // finalize the previous segment: its rows have landed (all but the newest group)
     if (prev_slot >= 0) {
@@ -614,19 +623,154 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
 // --------------------------------------------------------------------------
 // Phase 2, REPLAY warp
 // --------------------------------------------------------------------------
+// One decision round over up to 32 items in database order (lane order).
+// cand/fv: float32 candidate test input; f64/e64: exact scores if `have`,
+// else loaded here.  Returns the lane of the insertion (or -1); lanes up to
+// it (or all) are decided and recorded.
+struct Decided {
+  int first;       // inserting lane or -1
+  uint32_t done;   // lanes decided in this round
+};
+
+template <bool kCertified>
+__device__ __forceinline__ Decided decide_round(Live& L, const Ctx& c, int lane, bool cand,
+                                                float fv, int64_t id, bool& have, double& f64,
+                                                double& e64, uint32_t* surv) {
+  const ScanParams& p = *c.p;
+  const uint32_t cmask = __ballot_sync(0xffffffffu, cand);
+  Decided d{-1, 0xffffffffu};
+  if (!cmask) return d;
+  bool refined = false, certified = false;
+  if (cand) {
+    if (kCertified && !c.wide && fv < L.lo) {
+      refined = true;
+    } else {
+      if (!have) {
+        const Row r = load_row(p.codes_full, p.KP, id);
+        f64 = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
+        e64 = exact64(c.lut, p.m, p.K, c.pw, r);
+        have = true;
+      }
+      certified = true;
+      refined = f64 < L.thr64;
+    }
+    if (refined && !have) {
+      const Row r = load_row(p.codes_full, p.KP, id);
+      f64 = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
+      e64 = exact64(c.lut, p.m, p.K, c.pw, r);
+      have = true;
+    }
+  }
+  const bool ins = refined && (e64 < L.T64);
+  const uint32_t rmask = __ballot_sync(0xffffffffu, refined);
+  const uint32_t imask = __ballot_sync(0xffffffffu, ins);
+  const uint32_t cert = __ballot_sync(0xffffffffu, certified);
+  const int first = imask ? __ffs(imask) - 1 : 31;
+  const uint32_t decided = imask ? (0xffffffffu >> (31 - first)) : 0xffffffffu;
+  L.refinements += __popc(rmask & decided);
+  L.candidates += __popc(cmask & decided);
+  L.certified += __popc(cert & decided);
+  if (refined && ((decided >> lane) & 1u)) record_survivor(surv, id);
+  d.done = decided;
+  if (imask) {
+    d.first = first;
+    const double ne = __shfl_sync(0xffffffffu, e64, first);
+    const double nf = __shfl_sync(0xffffffffu, f64, first);
+    const int32_t nid = (int32_t)__shfl_sync(0xffffffffu, (int32_t)id, first);
+    L.H.replace_max(ne, nid, nf, lane);
+    live_update(L, p.F, p.sigma, c.wide);
+    ++L.insertions;
+  }
+  return d;
+}
+
+// Exact fallback for items >= pos of one segment: groups gated by their
+// minimum, float32 scores recomputed from the codes with this warp's own
+// page replicas, float64 scores from the rows.
+template <int FP>
+__device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint32_t sb,
+                                int64_t pos, uint32_t* surv) {
+  using G = Geo<FP>;
+  constexpr int IPC = G::IPC;
+  constexpr int GPB = 32 / IPC;  // groups per 32-lane batch
+  const ScanParams& p = *c.p;
+  const int64_t base = t * G::S;
+  const float* gmin = reinterpret_cast<const float*>(c.at(sb + p.so_gmin));
+  const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
+  uint32_t Lp[FP];
+#pragma unroll
+  for (int s = 0; s < FP; ++s)
+    Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
+            (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
+  ++L.fallback_segments;
+  // groups in 32-group rounds; only those holding items >= pos
+  const int g_first = (int)((pos - base) / IPC);
+  for (int r0 = (g_first / 32) * 32; r0 < G::NC; r0 += 32) {
+    const int gl = r0 + lane;
+    const float gv = gmin[gl];
+    uint32_t gm = __ballot_sync(0xffffffffu, gl >= g_first && (c.wide || gv < L.hi));
+    while (gm) {
+      const int gi = lane / IPC;
+      const int j = lane % IPC;
+      const int ngrp = min(GPB, __popc(gm));
+      const int mygrp = gi < ngrp ? (int)__fns(gm, 0, gi + 1) : -1;
+      int lastgrp = (int)__fns(gm, 0, ngrp);
+      const int cc = r0 + (mygrp < 0 ? 0 : mygrp);
+      const int64_t id = base + (int64_t)cc * IPC + j;
+      const bool valid = mygrp >= 0 && id >= pos && id < p.n;
+      // recompute the float32 fast score of this item from its code chunk
+      float fv = kInf;
+      if (valid) {
+        const uint4 x = __ldg(codes + t * G::NC + cc);
+        const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+        float acc = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < IPC; ++jj) {
+          if (jj == j) {
+            float a2[FP];
+#pragma unroll
+            for (int s = 0; s < FP; ++s) {
+              const int byte = jj * FP + s;
+              const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
+              a2[s] = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
+            }
+#pragma unroll
+            for (int h = 1; h < FP; h *= 2)
+#pragma unroll
+              for (int s = 0; s + h < FP; s += 2 * h) a2[s] = a2[s] + a2[s + h];
+            acc = a2[0];
+          }
+        }
+        fv = acc;
+      }
+      bool have = false;
+      double f64 = 0.0, e64 = 0.0;
+      uint32_t done = 0;
+      for (;;) {
+        const bool cand = valid && !((done >> lane) & 1u) && (c.wide || fv < L.hi);
+        const Decided d = decide_round<true>(L, c, lane, cand, fv, id, have, f64, e64, surv);
+        done |= d.done;
+        if (d.first < 0) break;
+        // threshold moved: cut the batch after the inserting item's group
+        const int gfirst = __shfl_sync(0xffffffffu, mygrp, d.first);
+        done |= __ballot_sync(0xffffffffu, mygrp > gfirst);
+        lastgrp = gfirst;
+      }
+      const uint32_t later = (lastgrp >= 31) ? 0u : (0xffffffffu << (lastgrp + 1));
+      gm = later & __ballot_sync(0xffffffffu, gl >= g_first && (c.wide || gv < L.hi));
+    }
+  }
+}
+
 template <int FP>
 __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int64_t seg0) {
   using G = Geo<FP>;
-  constexpr int IPC = G::IPC;
-  constexpr int S = G::S;
-  constexpr int GPB = 32 / IPC;  // groups per 32-lane batch
   const ScanParams& p = *c.p;
   const int F = p.F;
-  const int k = p.k;
   const int64_t n = p.n;
   const bool wide = c.wide;
   uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
-  const int ncache = kNS * p.cw;
+  const int cw = p.cw;
 
   int iter = 0;
   for (int64_t t = seg0; t < p.nseg; ++t, ++iter) {
@@ -636,121 +780,72 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
     mbar_wait(c.ctrl + 8 * slot, par);  // full[slot]
     L.wait_cycles += clock64() - tw;
     const uint32_t sb = p.off_slot[slot];
-    const float* wmin = reinterpret_cast<const float*>(c.at(sb + p.so_wmin));
-    const float* gmin = reinterpret_cast<const float*>(c.at(sb + p.so_gmin));
-    const uint16_t* rcidx = reinterpret_cast<const uint16_t*>(c.at(sb + p.so_rcidx));
-    const int32_t* eid = reinterpret_cast<const int32_t*>(c.at(sb + p.so_eid));
-    const double* ef64 = reinterpret_cast<const double*>(c.at(sb + p.so_ef64));
-    const double* ee64 = reinterpret_cast<const double*>(c.at(sb + p.so_ee64));
-    const int64_t base = t * S;
-
-    const float wmv = lane < kNS ? wmin[lane] : kInf;
-    uint32_t wmask = __ballot_sync(0xffffffffu, lane < kNS && (wide || wmv < L.hi));
-    while (wmask) {
-      const int w = __ffs(wmask) - 1;
-      // this warp's 64 groups, in item order: c = w*64 + v*32 + lane
-      const float g0 = gmin[w * 64 + lane];
-      const float g1 = gmin[w * 64 + 32 + lane];
-      uint64_t gm = (uint64_t)__ballot_sync(0xffffffffu, wide || g0 < L.hi) |
-                    ((uint64_t)__ballot_sync(0xffffffffu, wide || g1 < L.hi) << 32);
-      while (gm) {
-        // batch: the next GPB candidate groups, lane <-> (group gi, item j)
-        const int gi = lane / IPC;
-        const int j = lane % IPC;
-        const uint32_t lo32 = (uint32_t)gm, hi32 = (uint32_t)(gm >> 32);
-        const int nlo = __popc(lo32);
-        const int ngrp = min(GPB, nlo + __popc(hi32));
-        auto nth = [&](int q) {  // q-th set bit of gm (q < popc(gm))
-          return q < nlo ? (int)__fns(lo32, 0, q + 1) : 32 + (int)__fns(hi32, 0, q - nlo + 1);
-        };
-        int mygrp = gi < ngrp ? nth(gi) : -1;
-        int lastgrp = nth(ngrp - 1);
-        const int cc = w * 64 + (mygrp < 0 ? 0 : mygrp);
-        const int il = cc * IPC + j;
-        const int64_t id = base + il;
-        const bool valid = mygrp >= 0 && id >= k && id < n;
-        // fast score and the cache entry index are independent loads
-        const float fv = valid ? lds_f32(sb + (uint32_t)(j * kValStride + cc) * 4) : kInf;
-        const int e = (valid && ncache > 0) ? (int)rcidx[il] : ncache;
-        // cached float64 scores (precomputed by the scan warps); loaded
-        // speculatively next to the id check
-        double cf = 0.0, ce = 0.0;
-        bool cached = false;
-        if (e < ncache) {
-          const int32_t eidv = eid[e];
-          const double cfv = ef64[e], cev = ee64[e];
-          if (eidv == (int32_t)id) {
-            cached = true;
-            cf = cfv;
-            ce = cev;
-          }
+    const int64_t base = t * G::S;
+    const int64_t ins0 = L.insertions;
+    // per-warp meta (uniform): list length, threshold the list was cut at, minimum
+    const int32_t* meta = reinterpret_cast<const int32_t*>(c.at(sb));
+    const int mcnt = lane < kNS ? meta[lane] : 0;
+    const float mpub = lane < kNS ? __int_as_float(meta[8 + lane]) : kInf;
+    const float mwm = lane < kNS ? __int_as_float(meta[16 + lane]) : kInf;
+    auto incomplete = [&](float hi) {  // warps whose list may miss a candidate at hi
+      return __ballot_sync(0xffffffffu, lane < kNS && (wide || mwm < hi) &&
+                                            (wide || mpub < hi || mcnt > cw));
+    };
+    const uint32_t active = __ballot_sync(0xffffffffu, lane < kNS && (wide || mwm < L.hi));
+    if (active) {
+      if (incomplete(L.hi)) {
+        replay_fallback<FP>(L, c, lane, t, sb, base, surv);
+      } else {
+        // concatenated per-warp lists, in item order
+        const int clen = mcnt < cw ? mcnt : cw;
+        int incl = clen;
+#pragma unroll
+        for (int o = 1; o < kNS; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
-        uint32_t done = 0;
-        for (;;) {
-          const bool cand = valid && !((done >> lane) & 1u) && (wide || fv < L.hi);
-          const uint32_t cmask = __ballot_sync(0xffffffffu, cand);
-          if (!cmask) break;
-          bool refined = false;
-          bool certified = false;
-          double f64 = cf, e64 = ce;
-          if (cand) {
-            if (!wide && fv < L.lo) {
-              refined = true;
-            } else {
-              if (!cached) {
-                const Row r = load_row(p.codes_full, p.KP, id);
-                cf = f64 = fast64(c.lut, p.m, F, c.pw, p.fast_books, r);
-                ce = e64 = exact64(c.lut, p.m, p.K, c.pw, r);
-                cached = true;
-              }
-              certified = true;
-              refined = f64 < L.thr64;
-            }
-            if (refined && !cached) {
-              const Row r = load_row(p.codes_full, p.KP, id);
-              cf = f64 = fast64(c.lut, p.m, F, c.pw, p.fast_books, r);
-              ce = e64 = exact64(c.lut, p.m, p.K, c.pw, r);
-              cached = true;
+        const int total = __shfl_sync(0xffffffffu, incl, kNS - 1);
+        const int32_t* eid = reinterpret_cast<const int32_t*>(c.at(sb + p.so_eid));
+        const float* ef32 = reinterpret_cast<const float*>(c.at(sb + p.so_ef32));
+        const double* ef64 = reinterpret_cast<const double*>(c.at(sb + p.so_ef64));
+        const double* ee64 = reinterpret_cast<const double*>(c.at(sb + p.so_ee64));
+        int64_t fb_from = -1;  // fallback start after an insertion lifts the bound
+        for (int b0 = 0; b0 < total; b0 += 32) {
+          // lane -> (warp w, entry e) through the uniform prefix of list lengths
+          const int i = b0 + lane;
+          int w = 0, start_w = 0;
+#pragma unroll
+          for (int q = 0; q < kNS; ++q) {
+            const int iq = __shfl_sync(0xffffffffu, incl, q);  // inclusive end of warp q
+            const int sq = iq - __shfl_sync(0xffffffffu, clen, q);
+            if (i >= sq && i < iq) { w = q; start_w = sq; }
+          }
+          const bool valid = i < total;
+          const int ent = w * cw + (i - start_w);
+          const int64_t id = valid ? (int64_t)eid[ent] : 0;
+          const float fv = valid ? ef32[ent] : kInf;
+          double f64 = valid ? ef64[ent] : 0.0, e64 = valid ? ee64[ent] : 0.0;
+          bool have = true;
+          uint32_t done = 0;
+          for (;;) {
+            const bool cand = valid && !((done >> lane) & 1u) && (wide || fv < L.hi) && id < n;
+            const Decided d = decide_round<true>(L, c, lane, cand, fv, id, have, f64, e64, surv);
+            done |= d.done;
+            if (d.first < 0) break;
+            // the bound moved: lists cut at a lower threshold may now miss items
+            if (incomplete(L.hi)) {
+              fb_from = __shfl_sync(0xffffffffu, id, d.first) + 1;
+              break;
             }
           }
-          const bool ins = refined && (e64 < L.T64);
-          const uint32_t rmask = __ballot_sync(0xffffffffu, refined);
-          const uint32_t imask = __ballot_sync(0xffffffffu, ins);
-          const uint32_t cert = __ballot_sync(0xffffffffu, certified);
-          const int first = imask ? __ffs(imask) - 1 : 31;
-          const uint32_t decided = imask ? (0xffffffffu >> (31 - first)) : 0xffffffffu;
-          L.refinements += __popc(rmask & decided);
-          L.candidates += __popc(cmask & decided);
-          L.certified += __popc(cert & decided);
-          if (refined && ((decided >> lane) & 1u)) record_survivor(surv, id);
-          done |= decided;
-          if (!imask) break;
-          // insertion (search.py:152-154)
-          const double ne = __shfl_sync(0xffffffffu, e64, first);
-          const double nf = __shfl_sync(0xffffffffu, f64, first);
-          const int32_t nid = (int32_t)__shfl_sync(0xffffffffu, (int32_t)id, first);
-          L.H.replace_max(ne, nid, nf, lane);
-          live_update(L, c, F, p.sigma, wide, k, lane);
-          ++L.insertions;
-          // The threshold moved: groups after the inserting item's group were
-          // gated with the old one (and gated-out groups between batch members
-          // were skipped), so cut the batch here; later groups are re-gated.
-          const int gfirst = __shfl_sync(0xffffffffu, mygrp, first);
-          done |= __ballot_sync(0xffffffffu, mygrp > gfirst);
-          lastgrp = gfirst;
+          if (fb_from >= 0) break;
         }
-        // drop the processed groups; the bound may have moved either way, so
-        // re-test every later group of this warp against the live threshold
-        const uint64_t later = (lastgrp >= 63) ? 0ull : (~0ull << (lastgrp + 1));
-        gm = later & ((uint64_t)__ballot_sync(0xffffffffu, wide || g0 < L.hi) |
-                      ((uint64_t)__ballot_sync(0xffffffffu, wide || g1 < L.hi) << 32));
+        if (fb_from >= 0 && fb_from < base + G::S) replay_fallback<FP>(L, c, lane, t, sb, fb_from, surv);
       }
-      const uint32_t later_w = (w >= 31) ? 0u : (0xffffffffu << (w + 1));
-      wmask = later_w & __ballot_sync(0xffffffffu, lane < kNS && (wide || wmv < L.hi));
     }
     __syncwarp();
     mbar_arrive(c.ctrl + 32 + 8 * slot);  // empty[slot]
-    publish_prefetch(L, c, F, p.sigma, wide, lane);
+    if (L.insertions != ins0) publish_prefetch(L, c, F, p.sigma, wide, lane);
   }
 }
 
@@ -854,7 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
 
   Live L;
   L.refinements = L.insertions = L.candidates = L.certified = L.wait_cycles = 0;
-  L.t_score = L.t_decide = L.t_insert = 0;
+  L.t_score = L.t_decide = L.t_insert = L.fallback_segments = 0;
   L.H.k = k;
   L.H.reg = k <= 32 * kRegHeapRegs;
   L.H.he = c.he;
@@ -862,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   L.H.hi = c.hi;
   if (warp == 0) {
     L.H.load(lane);
-    live_update(L, c, F, p.sigma, c.wide, k, lane);
+    live_update(L, F, p.sigma, c.wide);
     publish_prefetch(L, c, F, p.sigma, c.wide, lane);
   }
   __syncthreads();
@@ -904,6 +999,8 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
       st[8] = L.t_score;
       st[9] = L.t_decide;
       st[10] = L.t_insert;
+      st[11] = L.fallback_segments;
+      st[12] = p.nseg - seg0;        // phase-2 segments
     }
   }
 }
@@ -932,32 +1029,29 @@ static bool plan_layout(ScanParams& p) {
   if (!place((uint32_t)k * 8, &p.off_heap_f)) return false;
   if (!place((uint32_t)k * 4, &p.off_heap_i)) return false;
   auto al16 = [](uint32_t x) { return (x + 15u) & ~15u; };
-  // slot sub-layout for a per-warp cache of `cw` rows
+  // slot sub-layout for per-warp candidate lists of `cw` entries
   auto slot_layout = [&](int cw) {
-    uint32_t o = al16(G::IPC * kValStride * 4);
-    p.so_gmin = o;   o = al16(o + kNC * 4);
-    p.so_wmin = o;   o = al16(o + 32 * 4);
-    p.so_ecnt = o;   o = al16(o + 32 * 4);
-    p.so_rcidx = o;  o = al16(o + G::S * 2);
+    uint32_t o = kMetaBytes;
+    p.so_gmin = o;   o = al16(o + G::NC * 4);
     p.so_eid = o;    o = al16(o + kNS * cw * 4);
+    p.so_ef32 = o;   o = al16(o + kNS * cw * 4);
     p.so_ef64 = o;   o = al16(o + kNS * cw * 8);
     p.so_ee64 = o;   o = al16(o + kNS * cw * 8);
     p.so_erow = o;   o = al16(o + kNS * cw * 16);
     return o;
   };
-  const int cw_pref[] = {64, 32, 16, 8, 0};
+  const int cw_pref[] = {64, 32, 16, 8};
   for (int nb = 3; nb >= 2; --nb) {
     for (int cw : cw_pref) {
-      if (p.KP < 4 && cw) continue;  // rows narrower than a cp.async unit: no cache
       Region a0 = A, b0 = B;
       const uint32_t sbytes = slot_layout(cw);
       bool ok = true;
       for (int s = 0; s < nb && ok; ++s) ok = place(sbytes, &p.off_slot[s]);
-      if (ok) {
+      int C = 2048;
+      while (C > 32 && (uint32_t)C * 16 > sbytes) C >>= 1;
+      if (ok && C >= 64) {
         p.nb = nb;
         p.cw = cw;
-        int C = 2048;
-        while (C > 32 && ((uint32_t)C * 16 > sbytes || C > G::S)) C >>= 1;
         p.dense_chunk = C;
         const uint32_t end = B.cur > pages_end ? B.cur : pages_end;
         p.smem_end = end;

@@ -26,7 +26,7 @@ struct ScanParams {
   double* scores;             // [Q*k]
   int64_t* refinements;       // [Q] or null
   uint32_t* survivors;        // [Q*words] or null
-  int64_t* stats;             // [Q*4] or null
+  int64_t* stats;             // [Q*kStats] or null
   int32_t* error;             // device error word
   int64_t n;
   int64_t nseg;
@@ -38,9 +38,11 @@ struct ScanParams {
   int32_t nb;                 // slots in the ring
   uint32_t off_lut64, off_heap_e, off_heap_f, off_heap_i, off_ctrl;
   uint32_t off_slot[4];
-  // sub-layout of one slot (byte offsets from the slot start)
-  uint32_t so_gmin, so_wmin, so_ecnt, so_rcidx, so_eid, so_ef64, so_ee64, so_erow;
-  int32_t cw;                 // cached candidate rows per scan warp per segment
+  // sub-layout of one slot (byte offsets from the slot start): per-warp meta
+  // (candidate count, filter threshold used, warp minimum), per-group minima,
+  // per-warp candidate lists (id, fast32, fast64, exact64, code row)
+  uint32_t so_gmin, so_eid, so_ef32, so_ef64, so_ee64, so_erow;
+  int32_t cw;                 // candidate list capacity per scan warp per segment
   int32_t dense_chunk;        // items per prologue chunk
   uint32_t smem_end;          // absolute end of the planned layout
   uint32_t dyn_bytes;

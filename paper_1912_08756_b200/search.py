@@ -33,7 +33,7 @@ STATS_FIELDS = 16
 STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
                "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide",
                "prologue_score_cycles", "prologue_decide_cycles", "prologue_insert_cycles",
-               "r11", "r12", "r13", "r14", "r15")
+               "fallback_segments", "phase2_segments", "r13", "r14", "r15")
 
 
 @dataclass
