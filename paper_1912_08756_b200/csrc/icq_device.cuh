@@ -47,6 +47,12 @@ __device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// Arrive on `a` when all of this thread's prior cp.async copies have landed
+// (pending count +1 now, -1 asynchronously: net zero, the phase also waits on
+// the copies).
+__device__ __forceinline__ void mbar_arrive_cp_async(uint32_t a) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"

@@ -302,8 +302,9 @@ struct Ctx {
   __device__ __forceinline__ uint8_t* at(uint32_t abs) const { return dsm + (abs - dbase); }
 };
 
-// ctrl block: [0,32) full[4]  [32,64) empty[4]  96 pub_thr  100 prologue flag
-constexpr uint32_t kCtrlBytes = 128;
+// ctrl block: [0,64) full[8]  [64,128) empty[8]  128 pub_thr  132 prologue flag
+constexpr uint32_t kCtrlBytes = 160;
+constexpr int kMaxSlots = 8;
 // slot meta block: cnt[8] int32, pub[8] float, wmin[8] float
 constexpr uint32_t kMetaBytes = 128;
 
@@ -345,7 +346,7 @@ __device__ __forceinline__ void publish_prefetch(const Live& L, const Ctx& c, in
   float lo2, hi2;
   certified_bounds(__dadd_rn(a, sigma * (kPubR + 1)), F, lo2, hi2);
   if (lane == 0) {
-    volatile float* pub = reinterpret_cast<volatile float*>(c.at(c.ctrl + 96));
+    volatile float* pub = reinterpret_cast<volatile float*>(c.at(c.ctrl + 128));
     *pub = wide ? kInf : fmaxf(hi2, L.hi);
   }
 }
@@ -365,9 +366,9 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
   const int64_t n = p.n;
   const int k = p.k;
   const int C = p.dense_chunk;
-  double* df = reinterpret_cast<double*>(c.at(p.off_slot[0]));
+  double* df = reinterpret_cast<double*>(c.at(p.off_slots));
   double* de = df + C;
-  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(c.at(c.ctrl + 100));
+  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(c.at(c.ctrl + 132));
   uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
   int64_t pos = k;
   int seg_ins = 0;
@@ -457,22 +458,6 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
 // Phase 2, SCAN warps
 // --------------------------------------------------------------------------
 template <int FP>
-__device__ __forceinline__ void scan_finalize(const Ctx& c, int slot, int w, int lane) {
-  const ScanParams& p = *c.p;
-  const uint32_t sb = p.off_slot[slot];
-  const int total = reinterpret_cast<const volatile int32_t*>(c.at(sb))[w];
-  const int cnt = total < p.cw ? total : p.cw;
-  const int e0 = w * p.cw;
-  double* ef64 = reinterpret_cast<double*>(c.at(sb + p.so_ef64));
-  double* ee64 = reinterpret_cast<double*>(c.at(sb + p.so_ee64));
-  for (int e = lane; e < cnt; e += 32) {
-    const Row r = smem_row(c.at(sb + p.so_erow + (uint32_t)(e0 + e) * 16), p.KP);
-    ef64[e0 + e] = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, r);
-    ee64[e0 + e] = exact64(c.lut, p.m, p.K, c.pw, r);
-  }
-}
-
-template <int FP>
 __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t seg0) {
   using G = Geo<FP>;
   constexpr int IPC = G::IPC;
@@ -489,7 +474,7 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
   const int cbase = w * 32 * V + lane;  // chunk (group) v of this lane: cbase + 32 v
   const int64_t nseg = p.nseg;
   const int rowb = p.KP < 4 ? 4 : p.KP;
-  const volatile float* pub = reinterpret_cast<const volatile float*>(c.at(c.ctrl + 96));
+  const volatile float* pub = reinterpret_cast<const volatile float*>(c.at(c.ctrl + 128));
 
   uint4 a[V], b[V];
 #pragma unroll
@@ -499,7 +484,6 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
                            : make_uint4(0, 0, 0, 0);
   }
   int iter = 0;
-  int prev_slot = -1;
   for (int64_t t = seg0; t < nseg; ++t, ++iter) {
     uint4 x[V];
 #pragma unroll
@@ -539,24 +523,18 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
         for (int j = 0; j < IPC; ++j)
           if (base + (int64_t)(cbase + 32 * v) * IPC + j >= p.n) f[v][j] = kInf;
     }
-    float gm[V];
     float lm = kInf;
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      gm[v] = f[v][0];
+    for (int v = 0; v < V; ++v)
 #pragma unroll
-      for (int j = 1; j < IPC; ++j) gm[v] = fminf(gm[v], f[v][j]);
-      lm = fminf(lm, gm[v]);
-    }
+      for (int j = 0; j < IPC; ++j) lm = fminf(lm, f[v][j]);
     // non-negative floats order like their bit patterns: one redux for the warp min
     const float wm = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(lm)));
 
     const int slot = iter % p.nb;
     const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
-    mbar_wait(c.ctrl + 32 + 8 * slot, par ^ 1u);  // empty[slot]
-    const uint32_t sb = p.off_slot[slot];
-#pragma unroll
-    for (int v = 0; v < V; ++v) sts_f32(sb + p.so_gmin + (uint32_t)(cbase + 32 * v) * 4, gm[v]);
+    mbar_wait(c.ctrl + 64 + 8 * slot, par ^ 1u);  // empty[slot]
+    const uint32_t sb = p.off_slots + (uint32_t)slot * p.slot_bytes;
 
     // ordered candidate list: items with f < pub, in item order (v, lane, j)
     const float pt = *pub;
@@ -602,22 +580,12 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
       reinterpret_cast<volatile float*>(meta)[8 + w] = pt;
       reinterpret_cast<volatile float*>(meta)[16 + w] = wm;
     }
-    cp_async_commit();
-    // finalize the previous segment: its rows have landed (all but the newest group)
-    if (prev_slot >= 0) {
-      cp_async_wait<1>();
-      __syncwarp();
-      scan_finalize<FP>(c, prev_slot, w, lane);
-      mbar_arrive(c.ctrl + 8 * prev_slot);  // full[prev]
-    }
-    prev_slot = slot;
+    // full[slot] completes once every scan thread arrived AND its row copies
+    // landed — the scan warps never wait for their own cp.async traffic
+    mbar_arrive_cp_async(c.ctrl + 8 * slot);
+    mbar_arrive(c.ctrl + 8 * slot);
   }
-  if (prev_slot >= 0) {
-    cp_async_wait<0>();
-    __syncwarp();
-    scan_finalize<FP>(c, prev_slot, w, lane);
-    mbar_arrive(c.ctrl + 8 * prev_slot);
-  }
+  cp_async_wait<0>();
 }
 
 // --------------------------------------------------------------------------
@@ -695,19 +663,50 @@ __device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint
   constexpr int GPB = 32 / IPC;  // groups per 32-lane batch
   const ScanParams& p = *c.p;
   const int64_t base = t * G::S;
-  const float* gmin = reinterpret_cast<const float*>(c.at(sb + p.so_gmin));
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   uint32_t Lp[FP];
 #pragma unroll
   for (int s = 0; s < FP; ++s)
     Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
+  // float32 fast score of item jj of a 16-byte code chunk (this lane's replica)
+  auto item_f32 = [&](const uint4& x, int jj) {
+    const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
+    float out = kInf;
+#pragma unroll
+    for (int j2 = 0; j2 < IPC; ++j2) {
+      if (j2 == jj) {
+        float a2[FP];
+#pragma unroll
+        for (int s = 0; s < FP; ++s) {
+          const int byte = j2 * FP + s;
+          const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
+          a2[s] = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
+        }
+#pragma unroll
+        for (int h = 1; h < FP; h *= 2)
+#pragma unroll
+          for (int s = 0; s + h < FP; s += 2 * h) a2[s] = a2[s] + a2[s + h];
+        out = a2[0];
+      }
+    }
+    return out;
+  };
   ++L.fallback_segments;
   // groups in 32-group rounds; only those holding items >= pos
   const int g_first = (int)((pos - base) / IPC);
   for (int r0 = (g_first / 32) * 32; r0 < G::NC; r0 += 32) {
     const int gl = r0 + lane;
-    const float gv = gmin[gl];
+    // this lane's group minimum over undecided items, recomputed from the codes
+    float gv = kInf;
+    {
+      const uint4 x = __ldg(codes + t * G::NC + gl);
+#pragma unroll
+      for (int jj = 0; jj < IPC; ++jj) {
+        const int64_t idj = base + (int64_t)gl * IPC + jj;
+        if (idj >= pos && idj < p.n) gv = fminf(gv, item_f32(x, jj));
+      }
+    }
     uint32_t gm = __ballot_sync(0xffffffffu, gl >= g_first && (c.wide || gv < L.hi));
     while (gm) {
       const int gi = lane / IPC;
@@ -719,30 +718,7 @@ __device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint
       const int64_t id = base + (int64_t)cc * IPC + j;
       const bool valid = mygrp >= 0 && id >= pos && id < p.n;
       // recompute the float32 fast score of this item from its code chunk
-      float fv = kInf;
-      if (valid) {
-        const uint4 x = __ldg(codes + t * G::NC + cc);
-        const uint32_t wd[4] = {x.x, x.y, x.z, x.w};
-        float acc = 0.f;
-#pragma unroll
-        for (int jj = 0; jj < IPC; ++jj) {
-          if (jj == j) {
-            float a2[FP];
-#pragma unroll
-            for (int s = 0; s < FP; ++s) {
-              const int byte = jj * FP + s;
-              const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
-              a2[s] = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
-            }
-#pragma unroll
-            for (int h = 1; h < FP; h *= 2)
-#pragma unroll
-              for (int s = 0; s + h < FP; s += 2 * h) a2[s] = a2[s] + a2[s + h];
-            acc = a2[0];
-          }
-        }
-        fv = acc;
-      }
+      const float fv = valid ? item_f32(__ldg(codes + t * G::NC + cc), j) : kInf;
       bool have = false;
       double f64 = 0.0, e64 = 0.0;
       uint32_t done = 0;
@@ -779,7 +755,7 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
     const long long tw = clock64();
     mbar_wait(c.ctrl + 8 * slot, par);  // full[slot]
     L.wait_cycles += clock64() - tw;
-    const uint32_t sb = p.off_slot[slot];
+    const uint32_t sb = p.off_slots + (uint32_t)slot * p.slot_bytes;
     const int64_t base = t * G::S;
     const int64_t ins0 = L.insertions;
     // per-warp meta (uniform): list length, threshold the list was cut at, minimum
@@ -807,8 +783,6 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
         const int total = __shfl_sync(0xffffffffu, incl, kNS - 1);
         const int32_t* eid = reinterpret_cast<const int32_t*>(c.at(sb + p.so_eid));
         const float* ef32 = reinterpret_cast<const float*>(c.at(sb + p.so_ef32));
-        const double* ef64 = reinterpret_cast<const double*>(c.at(sb + p.so_ef64));
-        const double* ee64 = reinterpret_cast<const double*>(c.at(sb + p.so_ee64));
         int64_t fb_from = -1;  // fallback start after an insertion lifts the bound
         for (int b0 = 0; b0 < total; b0 += 32) {
           // lane -> (warp w, entry e) through the uniform prefix of list lengths
@@ -824,8 +798,16 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
           const int ent = w * cw + (i - start_w);
           const int64_t id = valid ? (int64_t)eid[ent] : 0;
           const float fv = valid ? ef32[ent] : kInf;
-          double f64 = valid ? ef64[ent] : 0.0, e64 = valid ? ee64[ent] : 0.0;
-          bool have = true;
+          // float64 scores of current candidates from the row the scan warps
+          // copied into the slot (others are loaded on demand)
+          double f64 = 0.0, e64 = 0.0;
+          bool have = false;
+          if (valid && (wide || fv < L.hi)) {
+            const Row r = smem_row(c.at(sb + p.so_erow + (uint32_t)ent * 16), p.KP);
+            f64 = fast64(c.lut, p.m, F, c.pw, p.fast_books, r);
+            e64 = exact64(c.lut, p.m, p.K, c.pw, r);
+            have = true;
+          }
           uint32_t done = 0;
           for (;;) {
             const bool cand = valid && !((done >> lane) & 1u) && (wide || fv < L.hi) && id < n;
@@ -844,7 +826,7 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
       }
     }
     __syncwarp();
-    mbar_arrive(c.ctrl + 32 + 8 * slot);  // empty[slot]
+    mbar_arrive(c.ctrl + 64 + 8 * slot);  // empty[slot]
     if (L.insertions != ins0) publish_prefetch(L, c, F, p.sigma, wide, lane);
   }
 }
@@ -905,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   if (tid == 0) {
     for (int s = 0; s < p.nb; ++s) {
       mbar_init(c.ctrl + 8 * s, kNS * 32);   // full: every scan thread arrives
-      mbar_init(c.ctrl + 32 + 8 * s, 32);    // empty: every replay lane arrives
+      mbar_init(c.ctrl + 64 + 8 * s, 32);    // empty: every replay lane arrives
     }
   }
   c.wide = __syncthreads_or(bad) != 0;
@@ -1032,31 +1014,31 @@ static bool plan_layout(ScanParams& p) {
   // slot sub-layout for per-warp candidate lists of `cw` entries
   auto slot_layout = [&](int cw) {
     uint32_t o = kMetaBytes;
-    p.so_gmin = o;   o = al16(o + G::NC * 4);
     p.so_eid = o;    o = al16(o + kNS * cw * 4);
     p.so_ef32 = o;   o = al16(o + kNS * cw * 4);
-    p.so_ef64 = o;   o = al16(o + kNS * cw * 8);
-    p.so_ee64 = o;   o = al16(o + kNS * cw * 8);
     p.so_erow = o;   o = al16(o + kNS * cw * 16);
     return o;
   };
-  const int cw_pref[] = {64, 32, 16, 8};
-  for (int nb = 3; nb >= 2; --nb) {
+  // deepest ring first: the replay works off the scan by up to nb segments
+  const int cw_pref[] = {32, 16};
+  for (int nb = kMaxSlots; nb >= 2; --nb) {
     for (int cw : cw_pref) {
       Region a0 = A, b0 = B;
       const uint32_t sbytes = slot_layout(cw);
-      bool ok = true;
-      for (int s = 0; s < nb && ok; ++s) ok = place(sbytes, &p.off_slot[s]);
-      int C = 2048;
-      while (C > 32 && (uint32_t)C * 16 > sbytes) C >>= 1;
-      if (ok && C >= 64) {
-        p.nb = nb;
-        p.cw = cw;
-        p.dense_chunk = C;
-        const uint32_t end = B.cur > pages_end ? B.cur : pages_end;
-        p.smem_end = end;
-        p.dyn_bytes = end - kDynBase;
-        return true;
+      // the ring is one contiguous block; the prologue buffer aliases it
+      if (place(sbytes * nb, &p.off_slots)) {
+        int C = 2048;
+        while (C > 32 && (uint32_t)C * 16 > sbytes * nb) C >>= 1;
+        if (C >= 256) {
+          p.nb = nb;
+          p.cw = cw;
+          p.slot_bytes = sbytes;
+          p.dense_chunk = C;
+          const uint32_t end = B.cur > pages_end ? B.cur : pages_end;
+          p.smem_end = end;
+          p.dyn_bytes = end - kDynBase;
+          return true;
+        }
       }
       A = a0;
       B = b0;

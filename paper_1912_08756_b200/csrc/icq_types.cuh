@@ -37,11 +37,12 @@ struct ScanParams {
   int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
   int32_t nb;                 // slots in the ring
   uint32_t off_lut64, off_heap_e, off_heap_f, off_heap_i, off_ctrl;
-  uint32_t off_slot[4];
+  uint32_t off_slots;         // contiguous ring of nb slots (aliased by the prologue buffer)
+  uint32_t slot_bytes;
   // sub-layout of one slot (byte offsets from the slot start): per-warp meta
-  // (candidate count, filter threshold used, warp minimum), per-group minima,
-  // per-warp candidate lists (id, fast32, fast64, exact64, code row)
-  uint32_t so_gmin, so_eid, so_ef32, so_ef64, so_ee64, so_erow;
+  // (candidate count, filter threshold used, warp minimum), then per-warp
+  // candidate lists (id, fast32, code row)
+  uint32_t so_eid, so_ef32, so_erow;
   int32_t cw;                 // candidate list capacity per scan warp per segment
   int32_t dense_chunk;        // items per prologue chunk
   uint32_t smem_end;          // absolute end of the planned layout
