@@ -3,7 +3,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
 
-Workload: one BASELINE config (default c2 = configs[1]; c1..c5 selectable),
+Workload: one BASELINE config (default c4 = the 10M-item scan-bound config the
+north-star roofline target names; c1..c5 selectable with --config),
 seeded synthetic data (tools/workloads.py), books trained by the reference
 (bench_data/), database encoded on the GPU.  A step = one batch of queries
 through the hot path (K1 LUT build + fused scan/prune/refine/top-k kernel).
@@ -131,7 +132,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c2"),
+    ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c4"),
                     choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--sigma", type=float, default=None, help="override the learned margin")
@@ -155,17 +156,11 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from tools.workloads import build_database, load_books, queries
+    from tools.workloads import build_database, index_rule, load_books, queries
 
     w = CONFIGS[args.config]
     books, meta = load_books(w)
-    learned_fast = np.asarray(meta["learned_fast"], dtype=np.uint32)
-    if learned_fast.size == w.F:
-        fast, rule = learned_fast, "learned"
-    else:
-        fast, rule = np.arange(w.F, dtype=np.uint32), "first-F (SURVEY 8d: learned fast set %s)" % (
-            learned_fast.tolist())
-    sigma = float(meta["learned_sigma"]) if args.sigma is None else float(args.sigma)
+    fast, sigma, rule, sigma_rule = index_rule(w, meta, args.sigma)
 
     t0 = time.time()
     codes = build_database(w, books, sweeps=args.sweeps)
@@ -179,7 +174,7 @@ def main():
         "workload": f"{w.name}: n={w.n} d={w.d} K={w.K} m=256 |F|={w.F} k={w.k} "
                     f"queries={w.Q} batch={B} dist={w.dist}",
         "n": w.n, "d": w.d, "K": w.K, "m": 256, "F": w.F, "k": w.k, "batch": B,
-        "fast": fast.tolist(), "fast_rule": rule, "sigma": sigma,
+        "fast": fast.tolist(), "fast_rule": rule, "sigma": sigma, "sigma_rule": sigma_rule,
         "books": f"reference icq.train on {int(meta['train_rows'])} seeded rows, "
                  f"{int(meta['epochs'])} epoch(s), seed {int(meta['seed'])}",
         "seeds": {"train": SEED_TRAIN, "db": SEED_DB, "queries": SEED_QUERIES},

@@ -55,7 +55,7 @@ struct Geo {
   static constexpr int S = NC * IPC;                             // items per segment
 };
 
-constexpr int kPubR = 1;             // prefetch threshold covers the next kPubR insertions
+constexpr int kPubR = 3;             // prefetch threshold covers the next kPubR insertions
 constexpr int kDenseStopIns = 6;     // leave the prologue once a segment sees <= this many
 #define kInf (__int_as_float(0x7f800000))
 
@@ -208,12 +208,19 @@ struct WarpHeap {
   }
   __device__ __forceinline__ double top_e() const { return ue[0]; }
   __device__ __forceinline__ double top_f() const { return uf[0]; }
-  // max fast score over entries 0..R
+  // max fast score over entries 0..R (R < kRegHeapRegs: lane 0 holds them)
   __device__ __forceinline__ double top_fast_max(int R) const {
-    double a = uf[0];
+    double a = 0.0;
+    if (reg) {
+      a = f[0];
 #pragma unroll
-    for (int j = 1; j < kTopC; ++j)
-      if (j <= R && j < uc) a = fmax(a, uf[j]);
+      for (int j = 1; j < kRegHeapRegs; ++j)
+        if (j <= R && j < k) a = fmax(a, f[j]);
+      a = __shfl_sync(0xffffffffu, a, 0);
+    } else {
+      a = hf[0];
+      for (int j = 1; j <= R && j < k; ++j) a = fmax(a, hf[j]);
+    }
     return a;
   }
   __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
@@ -316,6 +323,7 @@ struct Live {
   int64_t wait_cycles;  // replay time spent waiting for the scan warps
   int64_t t_score, t_decide, t_insert;  // prologue breakdown (warp 0 clocks)
   int64_t fallback_segments;            // segments re-derived from the codes
+  int64_t t_active, t_fallback;         // phase-2 replay breakdown (clocks)
   WarpHeap H;
 };
 
@@ -535,6 +543,7 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
     const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
     mbar_wait(c.ctrl + 64 + 8 * slot, par ^ 1u);  // empty[slot]
     const uint32_t sb = p.off_slots + (uint32_t)slot * p.slot_bytes;
+    sts_f32(sb + p.so_lmin + (uint32_t)(w * 32 + lane) * 4, lm);
 
     // ordered candidate list: items with f < pub, in item order (v, lane, j)
     const float pt = *pub;
@@ -664,6 +673,7 @@ __device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint
   const ScanParams& p = *c.p;
   const int64_t base = t * G::S;
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
+  const float* lmin = reinterpret_cast<const float*>(c.at(sb + p.so_lmin));
   uint32_t Lp[FP];
 #pragma unroll
   for (int s = 0; s < FP; ++s)
@@ -697,16 +707,9 @@ __device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint
   const int g_first = (int)((pos - base) / IPC);
   for (int r0 = (g_first / 32) * 32; r0 < G::NC; r0 += 32) {
     const int gl = r0 + lane;
-    // this lane's group minimum over undecided items, recomputed from the codes
-    float gv = kInf;
-    {
-      const uint4 x = __ldg(codes + t * G::NC + gl);
-#pragma unroll
-      for (int jj = 0; jj < IPC; ++jj) {
-        const int64_t idj = base + (int64_t)gl * IPC + jj;
-        if (idj >= pos && idj < p.n) gv = fminf(gv, item_f32(x, jj));
-      }
-    }
+    // gate chunk gl by the minimum of the scan lane that produced it
+    // (chunk gl = w*32V + v*32 + l)
+    const float gv = lmin[(gl / (32 * G::V)) * 32 + (gl % 32)];
     uint32_t gm = __ballot_sync(0xffffffffu, gl >= g_first && (c.wide || gv < L.hi));
     while (gm) {
       const int gi = lane / IPC;
@@ -768,9 +771,11 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
                                             (wide || mpub < hi || mcnt > cw));
     };
     const uint32_t active = __ballot_sync(0xffffffffu, lane < kNS && (wide || mwm < L.hi));
+    const long long ta = clock64();
     if (active) {
       if (incomplete(L.hi)) {
         replay_fallback<FP>(L, c, lane, t, sb, base, surv);
+        L.t_fallback += clock64() - ta;
       } else {
         // concatenated per-warp lists, in item order
         const int clen = mcnt < cw ? mcnt : cw;
@@ -822,12 +827,17 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
           }
           if (fb_from >= 0) break;
         }
-        if (fb_from >= 0 && fb_from < base + G::S) replay_fallback<FP>(L, c, lane, t, sb, fb_from, surv);
+        if (fb_from >= 0 && fb_from < base + G::S) {
+          const long long tf = clock64();
+          replay_fallback<FP>(L, c, lane, t, sb, fb_from, surv);
+          L.t_fallback += clock64() - tf;
+        }
       }
     }
     __syncwarp();
     mbar_arrive(c.ctrl + 64 + 8 * slot);  // empty[slot]
     if (L.insertions != ins0) publish_prefetch(L, c, F, p.sigma, wide, lane);
+    if (active) L.t_active += clock64() - ta;
   }
 }
 
@@ -932,6 +942,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   Live L;
   L.refinements = L.insertions = L.candidates = L.certified = L.wait_cycles = 0;
   L.t_score = L.t_decide = L.t_insert = L.fallback_segments = 0;
+  L.t_active = L.t_fallback = 0;
   L.H.k = k;
   L.H.reg = k <= 32 * kRegHeapRegs;
   L.H.he = c.he;
@@ -983,6 +994,8 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
       st[10] = L.t_insert;
       st[11] = L.fallback_segments;
       st[12] = p.nseg - seg0;        // phase-2 segments
+      st[13] = L.t_active;           // replay cycles in segments with candidates
+      st[14] = L.t_fallback;         // ... of which in the exact fallback
     }
   }
 }
@@ -1014,6 +1027,7 @@ static bool plan_layout(ScanParams& p) {
   // slot sub-layout for per-warp candidate lists of `cw` entries
   auto slot_layout = [&](int cw) {
     uint32_t o = kMetaBytes;
+    p.so_lmin = o;   o = al16(o + kNS * 32 * 4);
     p.so_eid = o;    o = al16(o + kNS * cw * 4);
     p.so_ef32 = o;   o = al16(o + kNS * cw * 4);
     p.so_erow = o;   o = al16(o + kNS * cw * 16);

@@ -42,7 +42,7 @@ struct ScanParams {
   // sub-layout of one slot (byte offsets from the slot start): per-warp meta
   // (candidate count, filter threshold used, warp minimum), then per-warp
   // candidate lists (id, fast32, code row)
-  uint32_t so_eid, so_ef32, so_erow;
+  uint32_t so_lmin, so_eid, so_ef32, so_erow;  // so_lmin: per-lane minima (fallback gating)
   int32_t cw;                 // candidate list capacity per scan warp per segment
   int32_t dense_chunk;        // items per prologue chunk
   uint32_t smem_end;          // absolute end of the planned layout

@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from tools.workloads import CONFIGS, build_database, load_books, queries  # noqa: E402
+from tools.workloads import CONFIGS, build_database, index_rule, load_books, queries  # noqa: E402
 import paper_1912_08756_b200 as icqb  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -19,9 +19,7 @@ ap.add_argument("--sigma", type=float, default=None)
 args = ap.parse_args()
 w = CONFIGS[args.config]
 books, meta = load_books(w)
-lf = np.asarray(meta["learned_fast"])
-fast = lf if lf.size == w.F else np.arange(w.F, dtype=np.uint32)
-sigma = float(meta["learned_sigma"]) if args.sigma is None else args.sigma
+fast, sigma, _, _ = index_rule(w, meta, args.sigma)
 codes = build_database(w, books)
 Q = queries(w)[: args.nq]
 dev = icqb.DeviceIndex.from_device(books, codes, fast)

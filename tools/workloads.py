@@ -166,3 +166,29 @@ def queries(w: Workload, device="cuda"):
     import torch
 
     return sample_torch(w, w.Q, SEED_QUERIES, device).to(torch.float64)
+
+
+def index_rule(w: Workload, meta: dict, sigma_override: float | None = None):
+    """Index-construction rule, recorded with every result.
+
+    fast set: the learned one when it has the configured size, else the first
+    |F| books of the residual chain (they carry most of the energy).
+    sigma: the learned margin when the learned model has a fast set; when the
+    reference learned an empty fast set (psi = {} — c3, c4 here) its margin
+    belongs to no fast set and sigma = 0 is imposed (the learned value of
+    c1, c2, c5).  A sigma sweep is reported separately.
+    """
+    learned_fast = np.asarray(meta["learned_fast"], dtype=np.uint32)
+    learned_sigma = float(meta["learned_sigma"])
+    if learned_fast.size == w.F:
+        fast, frule = learned_fast, "learned"
+    else:
+        fast = np.arange(w.F, dtype=np.uint32)
+        frule = f"first {w.F} books (learned fast set {learned_fast.tolist()})"
+    if sigma_override is not None:
+        sigma, srule = float(sigma_override), "override"
+    elif learned_fast.size:
+        sigma, srule = learned_sigma, "learned"
+    else:
+        sigma, srule = 0.0, f"0 (learned fast set empty; learned sigma {learned_sigma:.4g} unused)"
+    return fast, sigma, frule, srule
