@@ -50,6 +50,17 @@ def _peaks():
     return 6650.0, 1965.0, "fallback"
 
 
+def _profiled_traffic(cfg: str):
+    """DRAM bytes per scan-kernel launch (dram__bytes_read.sum + write.sum) from
+    the committed ncu --set full summary of this config, scaled to the bench
+    batch; None when no capture is committed."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    z = json.loads(p.read_text()).get(cfg)
+    return None if z is None else z.get("dram_bytes_per_launch_at_bench_batch")
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -67,7 +78,7 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -130,7 +141,7 @@ def cpu_baseline(books, codes_host, fast, sigma, Qhost, k, nq, workers):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c4"),
                     choices=sorted(CONFIGS))
@@ -326,7 +337,7 @@ def main():
                     "wide_queries": int(stats[:, 7].sum().item()),
                     "recall_vs_exact": recall},
         "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": scan_gbs / hbm_peak, "traffic": None,
+                     "frac": scan_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),
                      "peak_kind": peak_kind,
                      "kernel": "icq_scan_kernel (K2-K5 fused)",
                      "algorithmic_bytes_per_launch": B * w.n * w.F,
