@@ -223,6 +223,20 @@ struct WarpHeap {
     }
     return a;
   }
+  // largest fast score over the whole heap (warp-uniform result)
+  __device__ __forceinline__ double max_fast_all(int lane) const {
+    double a = 0.0;
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kRegHeapRegs; ++r)
+        if (kRegHeapRegs * lane + r < k) a = fmax(a, f[r]);
+    } else {
+      for (int i = lane; i < k; i += 32) a = fmax(a, hf[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    return a;
+  }
   __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
     // 1. uniform top cache: drop entry 0, insert x if it ranks inside the prefix
     double le = ue[0];  // smallest cached entry (static indexing keeps it in registers)
@@ -384,6 +398,8 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
     const int64_t end = min(n, (pos / C + 1) * C);
     const int cnt = (int)(end - pos);
     const long long tc0 = clock64();
+    const double fcut = p.sigma == 0.0 ? *reinterpret_cast<volatile double*>(c.at(c.ctrl + 136))
+                                       : __longlong_as_double(0x7ff0000000000000LL);
     for (int i0 = 0; i0 < cnt; i0 += kThreads * 8) {
       Row rows[8];  // issue all row loads first, then score (one memory latency per round)
 #pragma unroll
@@ -395,8 +411,11 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
       for (int r = 0; r < 8; ++r) {
         const int i = i0 + tid + r * kThreads;
         if (i < cnt) {
-          df[i] = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, rows[r]);
-          de[i] = exact64(c.lut, p.m, p.K, c.pw, rows[r]);
+          const double fi = fast64(c.lut, p.m, p.F, c.pw, p.fast_books, rows[r]);
+          df[i] = fi;
+          // never refined in this chunk (fi >= every reachable bound): no exact score needed
+          de[i] = (fi < fcut || !(fcut == fcut)) ? exact64(c.lut, p.m, p.K, c.pw, rows[r])
+                                                 : __longlong_as_double(0x7ff0000000000000LL);
         }
       }
     }
@@ -404,39 +423,54 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
     const long long tc1 = clock64();
     L.t_score += tc1 - tc0;
     if (warp == 0) {
-      for (int b0 = 0; b0 < cnt; b0 += 32) {
-        // no refinement in the next 128 items -> skip them (4 independent loads)
-        if (b0 + 128 <= cnt) {
-          bool any = false;
+      // 128-item windows: the four 32-item sub-batches are tested together
+      // (independent ballots), so one serial round covers a whole window up
+      // to its first insertion (search.py:148-154 applied in order).
+      constexpr int U = 4;
+      for (int w0 = 0; w0 < cnt; w0 += 32 * U) {
+        double f[U], e[U];
+        bool valid[U];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) any |= df[b0 + u * 32 + lane] < L.thr64;
-          if (!__any_sync(0xffffffffu, any)) {
-            b0 += 96;
-            continue;
-          }
+        for (int u = 0; u < U; ++u) {
+          const int i = w0 + u * 32 + lane;
+          valid[u] = i < cnt;
+          f[u] = valid[u] ? df[i] : 0.0;
+          e[u] = valid[u] ? de[i] : 0.0;
         }
-        const int i = b0 + lane;
-        const bool valid = i < cnt;
-        const double f = valid ? df[i] : 0.0;
-        const double e = valid ? de[i] : 0.0;
-        const int64_t id = pos + i;
-        uint32_t done = 0;
+        uint32_t done[U] = {0, 0, 0, 0};
         for (;;) {
-          const bool refined = valid && !((done >> lane) & 1u) && (f < L.thr64);
-          const bool ins = refined && (e < L.T64);
-          const uint32_t rmask = __ballot_sync(0xffffffffu, refined);
-          const uint32_t imask = __ballot_sync(0xffffffffu, ins);
-          const int first = imask ? __ffs(imask) - 1 : 31;
-          const uint32_t decided = imask ? (0xffffffffu >> (31 - first)) : 0xffffffffu;
-          L.refinements += __popc(rmask & decided);
-          L.candidates += __popc(rmask & decided);
-          if (refined && ((decided >> lane) & 1u)) record_survivor(surv, id);
-          done |= decided;
-          if (!imask) break;
-          const double ne = __shfl_sync(0xffffffffu, e, first);
-          const double nf = __shfl_sync(0xffffffffu, f, first);
+          uint32_t rm[U], im[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool refined = valid[u] && !((done[u] >> lane) & 1u) && (f[u] < L.thr64);
+            rm[u] = __ballot_sync(0xffffffffu, refined);
+            im[u] = __ballot_sync(0xffffffffu, refined && (e[u] < L.T64));
+          }
+          int uf = U;  // first sub-batch holding an insertion
+#pragma unroll
+          for (int u = U - 1; u >= 0; --u)
+            if (im[u]) uf = u;
+          int first = 31;
+          double ne = 0.0, nf = 0.0;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            uint32_t dec = 0;
+            if (u < uf) dec = 0xffffffffu;
+            if (u == uf) {
+              first = __ffs(im[u]) - 1;
+              dec = 0xffffffffu >> (31 - first);
+              ne = __shfl_sync(0xffffffffu, e[u], first);
+              nf = __shfl_sync(0xffffffffu, f[u], first);
+            }
+            const int nr = __popc(rm[u] & dec);
+            L.refinements += nr;
+            L.candidates += nr;
+            if (surv && ((rm[u] & dec) >> lane & 1u)) record_survivor(surv, pos + w0 + u * 32 + lane);
+            done[u] |= dec;
+          }
+          if (uf == U) break;
           const long long ti0 = clock64();
-          L.H.replace_max(ne, (int32_t)(pos + b0 + first), nf, lane);
+          L.H.replace_max(ne, (int32_t)(pos + w0 + uf * 32 + first), nf, lane);
           live_update64(L, p.sigma);
           L.t_insert += clock64() - ti0;
           ++L.insertions;
@@ -444,6 +478,10 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
         }
       }
       L.t_decide += clock64() - tc1;
+      // sigma == 0: the bound never exceeds the heap's largest fast score, so
+      // items at or above it need no exact score in the next chunk
+      const double hmax = L.H.max_fast_all(lane);
+      if (lane == 0) *reinterpret_cast<volatile double*>(c.at(c.ctrl + 136)) = hmax;
       live_update(L, p.F, p.sigma, c.wide);
       publish_prefetch(L, c, p.F, p.sigma, c.wide, lane);
       // stop at a segment boundary once the insertion rate has dropped
@@ -491,8 +529,10 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
     b[v] = seg0 + 1 < nseg ? ldg_stream(codes + (seg0 + 1) * G::NC + cbase + 32 * v)
                            : make_uint4(0, 0, 0, 0);
   }
-  int iter = 0;
-  for (int64_t t = seg0; t < nseg; ++t, ++iter) {
+  int slot = 0;       // ring position and phase parity, advanced incrementally
+  uint32_t par = 0;   // (a runtime modulo costs ~80 cycles per segment)
+  for (int64_t t = seg0; t < nseg; ++t, slot = (slot + 1 == p.nb) ? 0 : slot + 1,
+               par ^= (slot == 0) ? 1u : 0u) {
     uint4 x[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -539,8 +579,6 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
     // non-negative floats order like their bit patterns: one redux for the warp min
     const float wm = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(lm)));
 
-    const int slot = iter % p.nb;
-    const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
     mbar_wait(c.ctrl + 64 + 8 * slot, par ^ 1u);  // empty[slot]
     const uint32_t sb = p.off_slots + (uint32_t)slot * p.slot_bytes;
     sts_f32(sb + p.so_lmin + (uint32_t)(w * 32 + lane) * 4, lm);
@@ -751,10 +789,10 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
   uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
   const int cw = p.cw;
 
-  int iter = 0;
-  for (int64_t t = seg0; t < p.nseg; ++t, ++iter) {
-    const int slot = iter % p.nb;
-    const uint32_t par = (uint32_t)(iter / p.nb) & 1u;
+  int slot = 0;
+  uint32_t par = 0;
+  for (int64_t t = seg0; t < p.nseg; ++t, slot = (slot + 1 == p.nb) ? 0 : slot + 1,
+               par ^= (slot == 0) ? 1u : 0u) {
     const long long tw = clock64();
     mbar_wait(c.ctrl + 8 * slot, par);  // full[slot]
     L.wait_cycles += clock64() - tw;
@@ -952,6 +990,8 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
     L.H.load(lane);
     live_update(L, F, p.sigma, c.wide);
     publish_prefetch(L, c, F, p.sigma, c.wide, lane);
+    const double hmax = L.H.max_fast_all(lane);
+    if (lane == 0) *reinterpret_cast<volatile double*>(c.at(c.ctrl + 136)) = hmax;
   }
   __syncthreads();
   const long long t_setup = clock64();
