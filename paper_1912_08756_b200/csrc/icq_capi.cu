@@ -5,6 +5,7 @@
 // layout of icq.data.SearchIndex (data.py:193-263).  Validation mirrors
 // search.py:47-58, :123-131 and data.py:145-176.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -285,6 +286,13 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   p.scores = scores;
   p.refinements = refine;
   p.exact_mode = exact ? 1 : 0;
+  {
+    static const int dbg = [] {
+      const char* s = getenv("ICQ_DEBUG");
+      return s ? atoi(s) : 0;
+    }();
+    p.debug = dbg;  // experiments only; results are not the reference's when set
+  }
   p.survivors = exact ? nullptr : survivors;
   p.stats = stats;
   p.error = h->err_dev;

@@ -63,6 +63,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
       : "memory");
 }
 
+// bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // --------------------------------------------------------------------------
 // streaming 16-byte code loads (read once per query; do not pollute L1)
 // --------------------------------------------------------------------------

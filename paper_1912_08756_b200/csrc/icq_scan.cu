@@ -57,6 +57,8 @@ struct Geo {
 
 constexpr int kPubR = 3;             // prefetch threshold covers the next kPubR insertions
 constexpr int kDenseStopIns = 6;     // leave the prologue once a segment sees <= this many
+constexpr int kReplayBlock = 4;      // segments the replay consumes per probe (< slots)
+constexpr int kPrefetchSeg = 6;      // L2 bulk-prefetch distance of the code stream (segments)
 #define kInf (__int_as_float(0x7f800000))
 
 // --------------------------------------------------------------------------
@@ -338,6 +340,7 @@ struct Live {
   int64_t t_score, t_decide, t_insert;  // prologue breakdown (warp 0 clocks)
   int64_t fallback_segments;            // segments re-derived from the codes
   int64_t t_active, t_fallback;         // phase-2 replay breakdown (clocks)
+  int64_t n_rounds;                     // prologue decision rounds
   WarpHeap H;
 };
 
@@ -439,6 +442,7 @@ __device__ __forceinline__ int64_t dense_prologue(const Ctx& c, Live& L, int tid
         }
         uint32_t done[U] = {0, 0, 0, 0};
         for (;;) {
+          ++L.n_rounds;
           uint32_t rm[U], im[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
@@ -543,6 +547,10 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
 #pragma unroll
       for (int v = 0; v < V; ++v) b[v] = ldg_stream(codes + (t + 2) * G::NC + cbase + 32 * v);
     }
+    // this warp's chunks of a segment are one contiguous 32*V*16-byte run:
+    // pull it into L2 kPrefetchSeg segments ahead so the register prefetch hits L2
+    if (lane == 0 && t + kPrefetchSeg < nseg)
+      prefetch_l2_bulk(codes + (t + kPrefetchSeg) * G::NC + w * 32 * V, 32 * V * 16);
     float f[V][IPC];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -564,12 +572,15 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
       }
     }
     const int64_t base = t * S;
-    if (base + S > p.n) {  // padding past n never enters the replay
+    // padding past n never enters the replay; only the last segment has any,
+    // and 32-bit local indices keep the (predicated) test cheap
+    const int nvalid = (int)min((int64_t)S, p.n - base);
+    if (nvalid < S) {
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
         for (int j = 0; j < IPC; ++j)
-          if (base + (int64_t)(cbase + 32 * v) * IPC + j >= p.n) f[v][j] = kInf;
+          if ((cbase + 32 * v) * IPC + j >= nvalid) f[v][j] = kInf;
     }
     float lm = kInf;
 #pragma unroll
@@ -589,20 +600,33 @@ __device__ __forceinline__ void scan_role(const Ctx& c, int w, int lane, int64_t
     if (__any_sync(0xffffffffu, lm < pt)) {
       int32_t* eid = reinterpret_cast<int32_t*>(c.at(sb + p.so_eid));
       float* ef32 = reinterpret_cast<float*>(c.at(sb + p.so_ef32));
+      // one lane prefix scan for all V chunks: per-chunk hit counts packed in
+      // kFB-bit fields (32 lanes * IPC hits fit), 5 shuffle steps in total
+      constexpr int kFB = 32 / V;
+      constexpr uint32_t kFM = (kFB == 32) ? 0xffffffffu : ((1u << kFB) - 1u);
+      uint32_t masks[V];
+      uint32_t packed = 0;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         uint32_t mask = 0;
 #pragma unroll
         for (int j = 0; j < IPC; ++j) mask |= (f[v][j] < pt ? 1u : 0u) << j;
-        const int my = __popc(mask);
-        int incl = my;  // inclusive scan over lanes
+        masks[v] = mask;
+        packed |= (uint32_t)__popc(mask) << (kFB * v);
+      }
+      uint32_t incl = packed;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        int pos = total + incl - my;
-        total += __shfl_sync(0xffffffffu, incl, 31);
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t excl = incl - packed;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uint32_t mask = masks[v];
+        int pos = total + (int)((excl >> (kFB * v)) & kFM);
+        total += (int)((tot >> (kFB * v)) & kFM);
         while (mask) {
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
@@ -780,6 +804,10 @@ __device__ void replay_fallback(Live& L, const Ctx& c, int lane, int64_t t, uint
 }
 
 template <int FP>
+__device__ void replay_segment(Live& L, const Ctx& c, int lane, int64_t t, uint32_t sb,
+                               uint32_t* surv);
+
+template <int FP>
 __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int64_t seg0) {
   using G = Geo<FP>;
   const ScanParams& p = *c.p;
@@ -789,16 +817,57 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
   uint32_t* surv = p.survivors ? p.survivors + (int64_t)blockIdx.x * p.words : nullptr;
   const int cw = p.cw;
 
-  int slot = 0;
-  uint32_t par = 0;
-  for (int64_t t = seg0; t < p.nseg; ++t, slot = (slot + 1 == p.nb) ? 0 : slot + 1,
-               par ^= (slot == 0) ? 1u : 0u) {
+  // Slots are consumed in blocks of kReplayBlock segments: all waits first,
+  // then ONE meta probe (lane -> (segment lane/8, scan warp lane%8)) decides
+  // whether anything in the block can hold a candidate under the live bound;
+  // blocks without candidates cost a few waits and one ballot.
+  const int kB = min(kReplayBlock, p.nb);  // never more slots than the ring holds
+  int slot0 = 0;
+  uint32_t par0 = 0;
+  for (int64_t t0 = seg0; t0 < p.nseg; t0 += kB) {
+    const int nblk = (int)min((int64_t)kB, p.nseg - t0);
     const long long tw = clock64();
-    mbar_wait(c.ctrl + 8 * slot, par);  // full[slot]
+    {
+      int s = slot0;
+      uint32_t pr = par0;
+      for (int j = 0; j < nblk; ++j) {
+        mbar_wait(c.ctrl + 8 * s, pr);  // full[s]
+        if (++s == p.nb) { s = 0; pr ^= 1u; }
+      }
+    }
     L.wait_cycles += clock64() - tw;
-    const uint32_t sb = p.off_slots + (uint32_t)slot * p.slot_bytes;
-    const int64_t base = t * G::S;
     const int64_t ins0 = L.insertions;
+    const int jl = lane >> 3;  // kNS == 8 warps per segment
+    int sl = slot0 + jl;
+    if (sl >= p.nb) sl -= p.nb;
+    const float pwm = jl < nblk ? __int_as_float(reinterpret_cast<const int32_t*>(
+                                      c.at(p.off_slots + (uint32_t)sl * p.slot_bytes))[16 + (lane & 7)])
+                                : kInf;
+    const bool any = __ballot_sync(0xffffffffu, jl < nblk && (wide || pwm < L.hi)) != 0 &&
+                     !(p.debug & 1);
+    for (int j = 0; j < nblk; ++j) {
+      if (any) replay_segment<FP>(L, c, lane, t0 + j, p.off_slots + (uint32_t)slot0 * p.slot_bytes,
+                                  surv);
+      __syncwarp();
+      mbar_arrive(c.ctrl + 64 + 8 * slot0);  // empty[slot]: hand the slot back at once
+      if (++slot0 == p.nb) { slot0 = 0; par0 ^= 1u; }
+    }
+    if (L.insertions != ins0) publish_prefetch(L, c, F, p.sigma, wide, lane);
+  }
+}
+
+// One segment of phase 2 in database order (called by the replay warp).
+template <int FP>
+__device__ void replay_segment(Live& L, const Ctx& c, int lane, int64_t t, uint32_t sb,
+                               uint32_t* surv) {
+  using G = Geo<FP>;
+  const ScanParams& p = *c.p;
+  const int F = p.F;
+  const int64_t n = p.n;
+  const bool wide = c.wide;
+  const int cw = p.cw;
+  {
+    const int64_t base = t * G::S;
     // per-warp meta (uniform): list length, threshold the list was cut at, minimum
     const int32_t* meta = reinterpret_cast<const int32_t*>(c.at(sb));
     const int mcnt = lane < kNS ? meta[lane] : 0;
@@ -815,27 +884,24 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
         replay_fallback<FP>(L, c, lane, t, sb, base, surv);
         L.t_fallback += clock64() - ta;
       } else {
-        // concatenated per-warp lists, in item order
-        const int clen = mcnt < cw ? mcnt : cw;
-        int incl = clen;
+        // concatenated per-warp lists, in item order; every lane reads the 8
+        // list lengths itself (uniform loads) to map lane -> (warp, entry)
+        int cnt8[kNS];
 #pragma unroll
-        for (int o = 1; o < kNS; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, kNS - 1);
+        for (int q = 0; q < kNS; ++q) cnt8[q] = min(meta[q], cw);
+        int total = 0;
+#pragma unroll
+        for (int q = 0; q < kNS; ++q) total += cnt8[q];
         const int32_t* eid = reinterpret_cast<const int32_t*>(c.at(sb + p.so_eid));
         const float* ef32 = reinterpret_cast<const float*>(c.at(sb + p.so_ef32));
         int64_t fb_from = -1;  // fallback start after an insertion lifts the bound
         for (int b0 = 0; b0 < total; b0 += 32) {
-          // lane -> (warp w, entry e) through the uniform prefix of list lengths
           const int i = b0 + lane;
-          int w = 0, start_w = 0;
+          int w = 0, start_w = 0, acc = 0;
 #pragma unroll
           for (int q = 0; q < kNS; ++q) {
-            const int iq = __shfl_sync(0xffffffffu, incl, q);  // inclusive end of warp q
-            const int sq = iq - __shfl_sync(0xffffffffu, clen, q);
-            if (i >= sq && i < iq) { w = q; start_w = sq; }
+            if (i >= acc && i < acc + cnt8[q]) { w = q; start_w = acc; }
+            acc += cnt8[q];
           }
           const bool valid = i < total;
           const int ent = w * cw + (i - start_w);
@@ -871,11 +937,8 @@ __device__ __forceinline__ void replay_role(const Ctx& c, Live& L, int lane, int
           L.t_fallback += clock64() - tf;
         }
       }
+      L.t_active += clock64() - ta;
     }
-    __syncwarp();
-    mbar_arrive(c.ctrl + 64 + 8 * slot);  // empty[slot]
-    if (L.insertions != ins0) publish_prefetch(L, c, F, p.sigma, wide, lane);
-    if (active) L.t_active += clock64() - ta;
   }
 }
 
@@ -980,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
   Live L;
   L.refinements = L.insertions = L.candidates = L.certified = L.wait_cycles = 0;
   L.t_score = L.t_decide = L.t_insert = L.fallback_segments = 0;
-  L.t_active = L.t_fallback = 0;
+  L.t_active = L.t_fallback = L.n_rounds = 0;
   L.H.k = k;
   L.H.reg = k <= 32 * kRegHeapRegs;
   L.H.he = c.he;
@@ -1036,6 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1) icq_scan_kernel(const ScanParams 
       st[12] = p.nseg - seg0;        // phase-2 segments
       st[13] = L.t_active;           // replay cycles in segments with candidates
       st[14] = L.t_fallback;         // ... of which in the exact fallback
+      st[15] = L.n_rounds;           // prologue decision rounds
     }
   }
 }

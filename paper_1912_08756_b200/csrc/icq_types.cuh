@@ -35,6 +35,7 @@ struct ScanParams {
   int32_t K, m, KP, F;
   int32_t k;
   int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
+  int32_t debug;              // experiments only (ICQ_DEBUG env): bit 0 = replay skips phase 2
   int32_t nb;                 // slots in the ring
   uint32_t off_lut64, off_heap_e, off_heap_f, off_heap_i, off_ctrl;
   uint32_t off_slots;         // contiguous ring of nb slots (aliased by the prologue buffer)

@@ -34,7 +34,7 @@ STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end
                "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide",
                "prologue_score_cycles", "prologue_decide_cycles", "prologue_insert_cycles",
                "fallback_segments", "phase2_segments", "replay_active_cycles",
-               "replay_fallback_cycles", "r15")
+               "replay_fallback_cycles", "prologue_rounds")
 
 
 @dataclass
