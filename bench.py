@@ -229,10 +229,20 @@ def main():
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     outs = []
+    L = icqb._native.lib()
+    L.icq_profile_read(None, None)  # drop anything recorded during warm-up
+    L.icq_profile_enable(1)  # CUDA events around each pipeline kernel, launch stream
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             outs.append(step(args.warmup + i, evs[i]))
         torch.cuda.synchronize()
+    L.icq_profile_enable(0)
+    import ctypes as _C
+
+    kms = (_C.c_double * 3)()
+    klaunch = _C.c_int32()
+    L.icq_profile_read(kms, _C.byref(klaunch))
+    t_pro_k, t_filter_k, t_replay_k = (x / 1e3 for x in kms)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -253,7 +263,10 @@ def main():
         nq_all = nq
     qps = nq_all / t_total
     lookups = nq * w.n * w.F
-    scan_gbs = lookups / t_scan / 1e9  # per-GPU scan kernel (this rank)
+    # the filter kernel streams the fast codes of items [P, n) of every query
+    p_mean = float(stats[:, 3].mean().item())
+    filter_bytes = nq * (w.n - p_mean) * w.F
+    filter_gbs = filter_bytes / t_filter_k / 1e9  # per-GPU filter kernel (this rank)
     hbm_peak, sm_max, peak_kind = _peaks()
     smem_peak_glps = 148 * 32 * sm_max * 1e6 / 1e9
 
@@ -328,23 +341,32 @@ def main():
         "scan_ms_per_step": t_scan / args.steps * 1e3,
         "pruning": {"refined_fraction": float(refine.mean().item() / w.n),
                     "insertions_per_query": float(stats[:, 0].mean().item()),
-                    "replay_candidates_per_query": float(stats[:, 1].mean().item()),
+                    "replay_live_candidates_per_query": float(stats[:, 1].mean().item()),
                     "f64_certified_per_query": float(stats[:, 2].mean().item()),
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),
                     "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
-                    "phase2_cycles_per_query": float(stats[:, 5].mean().item()),
-                    "replay_wait_cycles_per_query": float(stats[:, 6].mean().item()),
+                    "replay_cycles_per_query": float(stats[:, 5].mean().item()),
+                    "rescanned_slices": int(stats[:, 6].sum().item()),
                     "wide_queries": int(stats[:, 7].sum().item()),
+                    "prologue_f64_scored_per_query": float(stats[:, 8].mean().item()),
+                    "filter_candidates_per_query": float(stats[:, 9].mean().item()),
+                    "filter_pass_fraction": float(stats[:, 9].mean().item() / w.n),
                     "recall_vs_exact": recall},
-        "roofline": {"bound": "hbm", "achieved": scan_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": scan_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),
+        "roofline": {"bound": "hbm", "achieved": filter_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": filter_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),
                      "peak_kind": peak_kind,
-                     "kernel": "icq_scan_kernel (K2-K5 fused)",
-                     "algorithmic_bytes_per_launch": B * w.n * w.F,
-                     "smem_gather_frac": (lookups / t_scan / 1e9) / smem_peak_glps},
+                     "kernel": "icq_filter_kernel (K3: fast-code stream, fp32 gather, compaction)",
+                     "algorithmic_bytes_per_launch": filter_bytes / args.steps,
+                     "filter_ms_per_launch": t_filter_k / args.steps * 1e3,
+                     "filter_share_of_step": t_filter_k / t_total,
+                     "smem_gather_frac": (filter_bytes / t_filter_k / 1e9) / smem_peak_glps},
+        "kernels_ms_per_step": {"lut": t_lut / args.steps * 1e3,
+                                "prologue": t_pro_k / args.steps * 1e3,
+                                "filter": t_filter_k / args.steps * 1e3,
+                                "replay": t_replay_k / args.steps * 1e3},
         "clocks": clk.summary(),
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 4 * args.steps,
         "cpu_baseline": cpu,
         "setup_seconds": prep_s,
     }

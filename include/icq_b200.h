@@ -136,6 +136,17 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
                            double sigma, int32_t exact, int64_t* ids_host,
                            double* scores_host, int64_t* refine_host, int32_t* fallback_out);
 
+/* ---------------------------------------------------------------------------
+ * Instrumentation (bench / profiling only; not part of the reference surface).
+ * icq_profile_enable(1) makes every following search call record CUDA events
+ * on its launch stream around the three kernels of each batch (prologue,
+ * filter, replay).  icq_profile_read synchronizes those events and returns
+ * the summed device milliseconds per kernel (ms_out[3]) and the number of
+ * batches recorded, then clears the record.
+ * ------------------------------------------------------------------------- */
+icq_status icq_profile_enable(int32_t on);
+icq_status icq_profile_read(double* ms_out, int32_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

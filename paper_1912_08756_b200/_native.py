@@ -43,6 +43,8 @@ SIGNATURES = {
                                    _vp, C.POINTER(_i32), _vp]),
     "icq_search_host": (_i32, [_vp, _vp, _i32, _i32, C.c_double, _i32, _vp, _vp, _vp,
                                C.POINTER(_i32)]),
+    "icq_profile_enable": (_i32, [_i32]),
+    "icq_profile_read": (_i32, [C.POINTER(C.c_double), C.POINTER(_i32)]),
 }
 
 _lib = None

@@ -20,6 +20,12 @@ using namespace icq;
 
 static thread_local std::string g_err;
 
+// Kernel timing instrumentation (icq_profile_enable / icq_profile_read):
+// CUDA events recorded on the launch stream around each pipeline kernel.
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<cudaEvent_t> g_prof_events;  // groups of 4 per launch
+
 static icq_status fail(icq_status code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -111,7 +117,7 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
   h->K = K; h->m = m; h->d = d; h->F = F; h->n = n;
   h->KP = pow2_ceil(K);
   h->FP = F ? pow2_ceil(F) : 0;
-  h->n_pad = (n + 8191) / 8192 * 8192;
+  h->n_pad = (n + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
   memset(h->fast_books, 0, sizeof(h->fast_books));
   bool prefix = true;
   for (int s = 0; s < F; ++s) {
@@ -191,6 +197,33 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
 extern "C" {
 
 const char* icq_last_error(void) { return g_err.c_str(); }
+
+icq_status icq_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+  return ICQ_OK;
+}
+
+icq_status icq_profile_read(double* ms_out, int32_t* launches) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  double acc[3] = {0, 0, 0};
+  const int groups = (int)(g_prof_events.size() / 4);
+  for (int i = 0; i < groups; ++i) {
+    cudaEvent_t* e = &g_prof_events[4 * i];
+    if (cudaEventSynchronize(e[3]) != cudaSuccess)
+      return fail(ICQ_ERR_CUDA, "profile: event synchronize failed");
+    for (int j = 0; j < 3; ++j) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e[j], e[j + 1]);
+      acc[j] += ms;
+    }
+  }
+  for (cudaEvent_t e : g_prof_events) cudaEventDestroy(e);
+  g_prof_events.clear();
+  if (ms_out) for (int j = 0; j < 3; ++j) ms_out[j] = acc[j];
+  if (launches) *launches = groups;
+  return ICQ_OK;
+}
 
 int32_t icq_abi_version(void) { return 1; }
 
@@ -278,23 +311,9 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     const int64_t words = (h->n + 31) / 32;
     CUDA_TRY(cudaMemsetAsync(survivors, 0, (size_t)Q * words * sizeof(uint32_t), s));
   }
-  ScanParams p;
+  PipeParams p;
   memset(&p, 0, sizeof(p));
   p.codes_full = h->codes_full;
-  p.lut64 = lut;
-  p.ids = ids;
-  p.scores = scores;
-  p.refinements = refine;
-  p.exact_mode = exact ? 1 : 0;
-  {
-    static const int dbg = [] {
-      const char* s = getenv("ICQ_DEBUG");
-      return s ? atoi(s) : 0;
-    }();
-    p.debug = dbg;  // experiments only; results are not the reference's when set
-  }
-  p.survivors = exact ? nullptr : survivors;
-  p.stats = stats;
   p.error = h->err_dev;
   p.n = h->n;
   p.words = (h->n + 31) / 32;
@@ -302,6 +321,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   p.m = h->m;
   p.KP = h->KP;
   p.k = k;
+  p.exact_mode = exact ? 1 : 0;
   int FP;
   if (exact) {
     p.codes_fast = h->codes_full;
@@ -316,12 +336,106 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     memcpy(p.fast_books, h->fast_books, sizeof(p.fast_books));
     p.sigma = sigma;
   }
-  int unsupported = 0;
-  CUDA_TRY(launch_scan(p, FP, Q, s, &unsupported));
-  if (unsupported)
-    return fail(ICQ_ERR_UNSUPPORTED, "k=%d does not fit the on-chip heap for K=%d, m=%d", k, h->K,
-                h->m);
-  return ICQ_OK;
+  // ---- plan: sub-batches, ranges, unit order, candidate pool -------------
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  auto env_i = [](const char* name, int64_t dflt) {
+    const char* v = getenv(name);
+    return v ? (int64_t)atoll(v) : dflt;
+  };
+  const int Qmax = (int)env_i("ICQ_QBATCH", 2048);
+  const int Qb = Q < Qmax ? Q : Qmax;
+  const bool big = (int64_t)h->n * FP > (int64_t)48 << 20;  // fast stream larger than ~L2/2
+  p.range_major = big ? 1 : 0;
+  {
+    const int64_t units = 8LL * sms;
+    int64_t nr = (units + Qb - 1) / Qb;
+    if (nr < 1) nr = 1;
+    int64_t rs = (h->n + nr - 1) / nr;
+    if (big && rs > ((int64_t)4 << 20)) rs = (int64_t)4 << 20;
+    rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
+    p.RS = rs;
+    p.NR = (int32_t)((h->n + rs - 1) / rs);
+  }
+  p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 256);
+  p.pro_min = env_i("ICQ_PRO_MIN", 8192);
+  {
+    int64_t pm = h->n / 16;
+    if (pm < ((int64_t)1 << 18)) pm = (int64_t)1 << 18;
+    p.pro_max = env_i("ICQ_PRO_MAX", pm);
+  }
+  {
+    int64_t entries = (int64_t)Qb * h->n / 64;
+    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)128 << 20;
+    entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
+    p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
+  }
+  const int filter_ctas = (int)env_i("ICQ_FILTER_CTAS", sms);
+  // ---- stream-ordered scratch (pool cached across calls) -----------------
+  static std::once_flag pool_once;
+  std::call_once(pool_once, [] {
+    int dev = 0;
+    cudaMemPool_t mp;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t b_qs = al(sizeof(QState) * Qb);
+  const size_t b_he = al((size_t)Qb * k * 8), b_hi = al((size_t)Qb * k * 4);
+  const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint2));
+  const size_t b_top = 256;
+  const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
+  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl;
+  char* sc = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&sc, scratch, s));
+  {
+    char* o = sc;
+    p.qs = reinterpret_cast<QState*>(o); o += b_qs;
+    p.heap_e = reinterpret_cast<double*>(o); o += b_he;
+    p.heap_f = reinterpret_cast<double*>(o); o += b_he;
+    p.heap_i = reinterpret_cast<int32_t*>(o); o += b_hi;
+    p.pool = reinterpret_cast<uint2*>(o); o += b_pool;
+    p.pool_top = reinterpret_cast<int32_t*>(o); o += b_top;
+    p.slices = reinterpret_cast<int32_t*>(o);
+  }
+  icq_status st = ICQ_OK;
+  for (int q0 = 0; q0 < Q && st == ICQ_OK; q0 += Qb) {
+    const int nq = Q - q0 < Qb ? Q - q0 : Qb;
+    PipeParams b = p;
+    b.Q = nq;
+    b.lut64 = lut + (size_t)q0 * h->K * h->m;
+    b.ids = ids + (size_t)q0 * k;
+    b.scores = scores + (size_t)q0 * k;
+    b.refinements = refine ? refine + q0 : nullptr;
+    b.survivors = (!exact && survivors) ? survivors + (size_t)q0 * p.words : nullptr;
+    b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
+    cudaError_t e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
+    int unsupported = 0;
+    cudaEvent_t* ev = nullptr;
+    cudaEvent_t evs[4];
+    {
+      std::lock_guard<std::mutex> g(g_prof_mu);
+      if (g_prof_on) {
+        for (int j = 0; j < 4; ++j) {
+          cudaEventCreate(&evs[j]);
+          g_prof_events.push_back(evs[j]);
+        }
+        ev = evs;
+      }
+    }
+    if (e == cudaSuccess) e = launch_pipeline(b, FP, filter_ctas, s, &unsupported, ev);
+    if (e != cudaSuccess) st = fail(ICQ_ERR_CUDA, "search launch: %s", cudaGetErrorString(e));
+    else if (unsupported)
+      st = fail(ICQ_ERR_UNSUPPORTED, "k=%d does not fit the on-chip heap for K=%d, m=%d", k,
+                h->K, h->m);
+  }
+  cudaFreeAsync(sc, s);
+  return st;
 }
 
 icq_status icq_search_two_step(icq_index_t h, const double* q, int32_t Q, int32_t k, double sigma,
@@ -398,7 +512,7 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
   if (e2 != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e2));
   int32_t err = 0;
   CUDA_TRY(cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost));
-  if (err & 1) return fail(ICQ_ERR_CUDA, "scan kernel shared-memory layout check failed");
+  if (err & 1) return fail(ICQ_ERR_CUDA, "filter kernel shared-memory layout check failed");
   return ICQ_OK;
 }
 

@@ -1,0 +1,285 @@
+// icq_common.cuh — device pieces shared by the prologue, filter and replay
+// kernels: float64 row scores in the reference's order, the (exact, id) key,
+// the replay warp's heap, and the live threshold state.
+//
+// Reference semantics: search_two_step, /root/reference/pkg/src/icq/search.py:112-165
+//   heap seeded with ids 0..k-1 scored exactly                      (:141-143)
+//   element i >= k refined iff fast[i] < bound + sigma, where bound is the
+//   FAST score of the current heap maximum by (exact, id)            (:149, :154)
+//   inserted iff exact[i] < exact(heap max) (strict)                 (:152-153)
+//   result: the heap sorted ascending by (score, id)                 (:156)
+#pragma once
+
+#include "icq_types.cuh"
+
+namespace icq {
+
+#define kInf (__int_as_float(0x7f800000))
+
+// --------------------------------------------------------------------------
+// code rows and float64 scores in the reference's order (search.py:94)
+// --------------------------------------------------------------------------
+struct Row {
+  uint32_t w[4];
+  __device__ __forceinline__ uint32_t byte(int b) const {
+    const uint32_t x = (b < 4) ? w[0] : (b < 8) ? w[1] : (b < 12) ? w[2] : w[3];
+    return (x >> ((b & 3) * 8)) & 0xffu;
+  }
+};
+
+__device__ __forceinline__ Row load_row(const uint8_t* codes_full, int KP, int64_t id) {
+  Row r;
+  r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0;
+  const uint8_t* p = codes_full + id * KP;
+  if (KP == 16) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    r.w[0] = v.x; r.w[1] = v.y; r.w[2] = v.z; r.w[3] = v.w;
+  } else if (KP == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    r.w[0] = v.x; r.w[1] = v.y;
+  } else if (KP == 4) {
+    r.w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+  } else if (KP == 2) {
+    r.w[0] = __ldg(reinterpret_cast<const uint16_t*>(p));
+  } else {
+    r.w[0] = __ldg(p);
+  }
+  return r;
+}
+
+__device__ __forceinline__ double exact64(const double* lut, int m, int K, bool pw, const Row& r) {
+  return ref_row_sum(K, pw, [&](int b) { return lut[b * m + (int)r.byte(b)]; });
+}
+
+__device__ __forceinline__ double fast64(const double* lut, int m, int F, bool pw,
+                                         const uint8_t* fb, const Row& r) {
+  return ref_row_sum(F, pw, [&](int s) {
+    const int b = fb[s];
+    return lut[b * m + (int)r.byte(b)];
+  });
+}
+
+// (exact, id) ordering of the reference heap (search.py:140: keys (-exact, -id))
+__device__ __forceinline__ bool key_gt(double e1, int32_t i1, double e2, int32_t i2) {
+  // branch-free (no short-circuit): the replay warp's hot compares must not
+  // open divergence regions
+  const bool gt = e1 > e2, eq = e1 == e2, ig = i1 > i2;
+  return gt | (eq & ig);
+}
+
+// Replace the maximum (entry 0) of a descending-sorted heap in shared memory.
+static __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int k, double e,
+                                        int32_t id, double f, int lane) {
+  int g = 0;
+  for (int base = 1; base < k; base += 32) {
+    const int i = base + lane;
+    const bool gt = (i < k) && key_gt(he[i < k ? i : 0], hi[i < k ? i : 0], e, id);
+    g += __popc(__ballot_sync(0xffffffffu, gt));
+  }
+  for (int base = 0; base < g; base += 32) {
+    const int i = base + lane;
+    double te = 0, tf = 0;
+    int32_t ti = 0;
+    if (i < g) { te = he[i + 1]; tf = hf[i + 1]; ti = hi[i + 1]; }
+    __syncwarp();
+    if (i < g) { he[i] = te; hf[i] = tf; hi[i] = ti; }
+    __syncwarp();
+  }
+  if (lane == 0) { he[g] = e; hf[g] = f; hi[g] = id; }
+  __syncwarp();
+}
+
+// The replay warp's view of the heap: the k best (exact, id) entries sorted
+// descending (entry 0 = heap maximum, search.py:140).  For k <= 128 the
+// entries live in warp registers in a BLOCKED layout (lane l holds entries
+// 4l..4l+3): an insertion shifts registers locally, moves only the lane
+// boundary entry with one shuffle per field, and finds its position with one
+// __reduce_add_sync.  Larger k keeps the sorted array in shared memory.  A
+// warp-uniform copy of the top two entries gives the new maximum (T and
+// bound) after an insertion with plain per-lane ALU work.
+constexpr int kRegHeapRegs = 4;
+constexpr int kTopC = 2;
+struct WarpHeap {
+  int k;
+  bool reg;
+  double e[kRegHeapRegs], f[kRegHeapRegs];
+  int32_t id[kRegHeapRegs];
+  double* he;
+  double* hf;
+  int32_t* hi;
+  double ue[kTopC], uf[kTopC];
+  int32_t ui[kTopC];
+  int uc;
+
+  __device__ __forceinline__ void load(int lane) {
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kRegHeapRegs; ++r) {
+        const int i = kRegHeapRegs * lane + r;
+        e[r] = i < k ? he[i] : 0.0;
+        f[r] = i < k ? hf[i] : 0.0;
+        id[r] = i < k ? hi[i] : 0;
+      }
+    }
+    refill();
+  }
+  __device__ __forceinline__ void store(int lane) {
+    if (!reg) return;
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = kRegHeapRegs * lane + r;
+      if (i < k) { he[i] = e[r]; hf[i] = f[r]; hi[i] = id[r]; }
+    }
+    __syncwarp();
+  }
+  __device__ __forceinline__ void refill() {
+#pragma unroll
+    for (int j = 0; j < kTopC; ++j) {
+      if (reg) {  // entries 0..kTopC-1 sit in lane 0 (kTopC <= kRegHeapRegs)
+        ue[j] = __shfl_sync(0xffffffffu, e[j], 0);
+        uf[j] = __shfl_sync(0xffffffffu, f[j], 0);
+        ui[j] = __shfl_sync(0xffffffffu, id[j], 0);
+      } else {
+        ue[j] = j < k ? he[j] : 0.0;
+        uf[j] = j < k ? hf[j] : 0.0;
+        ui[j] = j < k ? hi[j] : 0;
+      }
+    }
+    uc = k < kTopC ? k : kTopC;
+  }
+  __device__ __forceinline__ double top_e() const { return ue[0]; }
+  __device__ __forceinline__ double top_f() const { return uf[0]; }
+  // largest fast score over the whole heap (warp-uniform result)
+  __device__ __forceinline__ double max_fast_all(int lane) const {
+    double a = -__longlong_as_double(0x7ff0000000000000LL);
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kRegHeapRegs; ++r)
+        if (kRegHeapRegs * lane + r < k) a = fmax(a, f[r]);
+    } else {
+      for (int i = lane; i < k; i += 32) a = fmax(a, hf[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    return a;
+  }
+  // true when some heap fast score is NaN (fmax would hide it)
+  __device__ __forceinline__ bool any_nan_fast(int lane) const {
+    bool bad = false;
+    if (reg) {
+#pragma unroll
+      for (int r = 0; r < kRegHeapRegs; ++r)
+        if (kRegHeapRegs * lane + r < k) bad |= !(f[r] == f[r]);
+    } else {
+      for (int i = lane; i < k; i += 32) bad |= !(hf[i] == hf[i]);
+    }
+    return __any_sync(0xffffffffu, bad);
+  }
+  __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
+    // 1. uniform top cache: drop entry 0, insert x if it ranks inside the prefix
+    double le = ue[0];
+    int32_t li = ui[0];
+#pragma unroll
+    for (int j = 1; j < kTopC; ++j)
+      if (j == uc - 1) { le = ue[j]; li = ui[j]; }
+    const bool in = uc >= 2 && key_gt(xe, xid, le, li);
+#pragma unroll
+    for (int j = 0; j < kTopC; ++j) {
+      const int jn = j + 1 < kTopC ? j + 1 : j;
+      const bool above_gt = (j + 1 < uc) && key_gt(ue[jn], ui[jn], xe, xid);
+      const bool here_gt = j == 0 ? true : ((j < uc) && key_gt(ue[j], ui[j], xe, xid));
+      if (above_gt) { ue[j] = ue[jn]; uf[j] = uf[jn]; ui[j] = ui[jn]; }
+      else if (here_gt && in) { ue[j] = xe; uf[j] = xf; ui[j] = xid; }
+    }
+    if (!in) --uc;
+    // 2. the full sorted array (lanes or shared memory)
+    replace_max_array(xe, xid, xf, lane);
+    if (uc < 2 && k >= 2) refill();
+    if (k == 1) { ue[0] = xe; uf[0] = xf; ui[0] = xid; uc = 1; }
+  }
+  __device__ __forceinline__ void replace_max_array(double xe, int32_t xid, double xf, int lane) {
+    if (!reg) {
+      heap_replace_max(he, hf, hi, k, xe, xid, xf, lane);
+      return;
+    }
+    int cnt = 0;  // this lane's entries among 1..k-1 that stay above x
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = kRegHeapRegs * lane + r;
+      cnt += ((i >= 1) & (i < k) & key_gt(e[r], id[r], xe, xid)) ? 1 : 0;
+    }
+    const int g = __reduce_add_sync(0xffffffffu, cnt);  // sorted: they are entries 1..g
+    const double ne = __shfl_down_sync(0xffffffffu, e[0], 1);
+    const double nf = __shfl_down_sync(0xffffffffu, f[0], 1);
+    const int32_t ni = __shfl_down_sync(0xffffffffu, id[0], 1);
+#pragma unroll
+    for (int r = 0; r < kRegHeapRegs; ++r) {
+      const int i = kRegHeapRegs * lane + r;
+      const int rn = r + 1 < kRegHeapRegs ? r + 1 : r;
+      const double se = r + 1 < kRegHeapRegs ? e[rn] : ne;
+      const double sf = r + 1 < kRegHeapRegs ? f[rn] : nf;
+      const int32_t si = r + 1 < kRegHeapRegs ? id[rn] : ni;
+      if (i < g) { e[r] = se; f[r] = sf; id[r] = si; }
+      else if (i == g) { e[r] = xe; f[r] = xf; id[r] = xid; }
+    }
+  }
+};
+
+// Replay state (one warp; warp-uniform registers)
+struct Live {
+  double T64, bound64, thr64;
+  float lo, hi;
+  int64_t refinements, insertions, candidates, certified;
+  WarpHeap H;
+};
+
+__device__ __forceinline__ void live_update64(Live& L, double sigma) {
+  L.T64 = L.H.top_e();
+  L.bound64 = L.H.top_f();
+  L.thr64 = __dadd_rn(L.bound64, sigma);  // search.py:149 `bound + sigma`
+}
+
+// + certified float32 thresholds of "fast64 < thr64"
+__device__ __forceinline__ void live_update(Live& L, int F, double sigma, bool wide) {
+  live_update64(L, sigma);
+  if (wide) {
+    L.lo = -kInf;
+    L.hi = kInf;
+  } else {
+    certified_bounds(L.thr64, F, L.lo, L.hi);
+  }
+}
+
+// Stale filter threshold valid for EVERY later item:
+//  sigma == 0: M = max fast over the heap never increases (an inserted item
+//              has fast < bound <= M), and bound <= M;
+//  sigma  > 0: U = max(M, T - Smin) never increases (inserted x: fast(x) <=
+//              exact(x) - Smin < T - Smin) and bound <= U; filter at U + sigma.
+// Returns the float32 value `hi` with x32 >= hi  =>  fast64 >= every future
+// bound + sigma, i.e. an item is a candidate iff x32 < hi.
+__device__ __forceinline__ float stale_filter_hi(const Live& L, int F, double sigma, double smin,
+                                                 bool wide, int lane) {
+  if (wide) return kInf;
+  const double M = L.H.max_fast_all(lane);
+  if (L.H.any_nan_fast(lane)) return kInf;
+  double thr;
+  if (sigma == 0.0) {
+    thr = M;
+  } else {
+    // (T - Smin) with float64 slack for the different summation orders of
+    // fast and exact scores (relative 1e-12 >> K * 2^-53)
+    const double ts = __dsub_ru(L.T64, smin);
+    const double u = fmax(M, __dadd_ru(ts, fabs(L.T64) * 1e-12));
+    thr = __dadd_ru(u, sigma);
+  }
+  if (!(thr == thr)) return kInf;
+  float lo, hi;
+  certified_bounds(thr, F, lo, hi);
+  return hi;
+}
+
+__device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {
+  if (surv) atomicOr(surv + (id >> 5), 1u << (id & 31));
+}
+
+}  // namespace icq

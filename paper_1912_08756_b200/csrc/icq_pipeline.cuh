@@ -1,0 +1,872 @@
+// icq_pipeline.cuh — the ICQ two-step query path as three kernels per batch.
+// (templates; instantiated per fast-row width in icq_pipe_fp*.cu, dispatched
+// by icq_pipeline.cu)
+//
+// Reference: search_two_step, /root/reference/pkg/src/icq/search.py:112-165
+// (search_exact :97-109 is the same pipeline with the fast set = all books and
+// sigma = 0: then fast == exact and the prune predicate is the top-k test).
+//
+// The reference walks the database in order with a heap whose FAST score of
+// the maximum is the pruning bound (:149).  That chain is sequential, but the
+// bound is dominated by a monotone stale threshold (see
+// stale_filter_hi): once the heap has settled, one threshold is valid for
+// every later item, so the streaming part can run on all SMs at once and
+// only the few items below it need the in-order replay.
+//
+//   K2 icq_prologue_kernel  one CTA per query: the insertion-heavy start of
+//        the database, in order, until a block passes <= 1/pro_div of its
+//        items under the stale threshold.  fp32 prefilter (non-replicated
+//        table), float64 scores of the prefiltered items, warp-0 decisions in
+//        float64.  Leaves the heap, the refinement count and the fp32
+//        filter threshold `hi` for the rest.
+//   K3 icq_filter_kernel    the hot path: every SM streams fast-code bytes
+//        (16-byte loads, register double buffer + L2 bulk prefetch), gathers
+//        |F| fp32 entries per item from lane-private replicated LUT pages
+//        (one byte_perm per lookup, bank-conflict free) and compacts items
+//        with x32 < hi, in item order, into per-(query, range, warp) slices
+//        of a paged candidate pool.  No sequential dependency at all.
+//   K4 icq_replay_kernel    one warp per query: resumes the reference loop at
+//        the prologue end over the candidate slices in database order
+//        against the LIVE bound (certified fp32 test, float64 for the items
+//        it refines), heap insertions, output sorted by (score, id).  A slice
+//        whose candidates overflowed its pages is rescanned from the codes.
+//
+// Every decision compares the reference's float64 values, so ids, scores,
+// refinement counts and survivor sets are bitwise the reference's.
+#pragma once
+#include "icq_common.cuh"
+
+namespace icq {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// --------------------------------------------------------------------------
+// decision context shared by the prologue and replay warps
+// --------------------------------------------------------------------------
+struct RCtx {
+  const double* lut;  // float64 LUT [K][m] in shared memory
+  const uint8_t* codes_full;
+  const uint8_t* fb;  // fast books
+  int KP, m, K, F;
+  double sigma;
+  bool pw, wide;
+  uint32_t* surv;
+};
+
+struct Decided {
+  int first;      // inserting lane or -1
+  uint32_t done;  // lanes decided in this round
+};
+
+// One decision round over up to 32 items in database order (lane order):
+// search.py:149-154 applied until the first insertion.
+__device__ __forceinline__ Decided decide_round(Live& L, const RCtx& c, int lane, bool cand,
+                                                float fv, int32_t id, bool& have, double& f64,
+                                                double& e64) {
+  const uint32_t cmask = __ballot_sync(kFull, cand);
+  Decided d{-1, kFull};
+  if (!cmask) return d;
+  bool refined = false, certified = false;
+  if (cand) {
+    if (!c.wide && fv < L.lo) {
+      refined = true;
+    } else {
+      if (!have) {
+        const Row r = load_row(c.codes_full, c.KP, id);
+        f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
+        e64 = exact64(c.lut, c.m, c.K, c.pw, r);
+        have = true;
+      }
+      certified = true;
+      refined = f64 < L.thr64;
+    }
+    if (refined && !have) {
+      const Row r = load_row(c.codes_full, c.KP, id);
+      f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
+      e64 = exact64(c.lut, c.m, c.K, c.pw, r);
+      have = true;
+    }
+  }
+  const bool ins = refined && (e64 < L.T64);
+  const uint32_t rmask = __ballot_sync(kFull, refined);
+  const uint32_t imask = __ballot_sync(kFull, ins);
+  const uint32_t cert = __ballot_sync(kFull, certified);
+  const int first = imask ? __ffs(imask) - 1 : 31;
+  const uint32_t decided = imask ? (kFull >> (31 - first)) : kFull;
+  L.refinements += __popc(rmask & decided);
+  L.candidates += __popc(cmask & decided);
+  L.certified += __popc(cert & decided);
+  if (refined && ((decided >> lane) & 1u)) record_survivor(c.surv, id);
+  d.done = decided;
+  if (imask) {
+    d.first = first;
+    const double ne = __shfl_sync(kFull, e64, first);
+    const double nf = __shfl_sync(kFull, f64, first);
+    const int32_t nid = __shfl_sync(kFull, id, first);
+    L.H.replace_max(ne, nid, nf, lane);
+    live_update(L, c.F, c.sigma, c.wide);
+    ++L.insertions;
+  }
+  return d;
+}
+
+// --------------------------------------------------------------------------
+// shared-memory layouts
+// --------------------------------------------------------------------------
+struct ProLayout {
+  uint32_t lut64, lut32, he, hf, hi, cf, ce, cid, ctrl, total;
+};
+__host__ __device__ inline uint32_t al16(uint32_t x) { return (x + 15u) & ~15u; }
+__host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
+  ProLayout L;
+  uint32_t o = 0;
+  L.lut64 = o; o = al16(o + (uint32_t)K * m * 8);
+  L.lut32 = o; o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 4);
+  L.he = o;    o = al16(o + (uint32_t)k * 8);
+  L.hf = o;    o = al16(o + (uint32_t)k * 8);
+  L.hi = o;    o = al16(o + (uint32_t)k * 4);
+  L.cf = o;    o = al16(o + kProBlock * 8);
+  L.ce = o;    o = al16(o + kProBlock * 8);
+  L.cid = o;   o = al16(o + kProBlock * 4);
+  L.ctrl = o;  o = al16(o + 128);
+  L.total = o;
+  return L;
+}
+
+constexpr int kWU = 8;  // replay window: kWU x 32 entries
+struct RepLayout {
+  uint32_t lut64, lut32, he, hf, hi, wid, wfv, widx, total;
+};
+__host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
+  RepLayout L;
+  uint32_t o = 0;
+  L.lut64 = o; o = al16(o + (uint32_t)K * m * 8);
+  L.lut32 = o; o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 4);
+  L.he = o;    o = al16(o + (uint32_t)k * 8);
+  L.hf = o;    o = al16(o + (uint32_t)k * 8);
+  L.hi = o;    o = al16(o + (uint32_t)k * 4);
+  L.wid = o;   o = al16(o + kWU * 32 * 4);
+  L.wfv = o;   o = al16(o + kWU * 32 * 4);
+  L.widx = o;  o = al16(o + kWU * 32 * 4);
+  L.total = o;
+  return L;
+}
+
+// float64 min over the non-fast books' LUT rows, rounded down (U threshold)
+static __device__ double smin_rd(const double* lut, int K, int m, const uint8_t* fb, int F, int lane) {
+  double s = 0.0;
+  for (int b = 0; b < K; ++b) {
+    bool fast = false;
+    for (int t = 0; t < F; ++t) fast |= fb[t] == b;
+    if (fast) continue;
+    double mn = __longlong_as_double(0x7ff0000000000000LL);
+    for (int j = lane; j < m; j += 32) mn = fmin(mn, lut[b * m + j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+    s = __dadd_rd(s, mn);
+  }
+  return s;
+}
+
+// ==========================================================================
+// K2: prologue
+// ==========================================================================
+template <int FP>
+__global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_constant__ PipeParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = blockIdx.x;
+  const int K = p.K, m = p.m, F = p.F, k = p.k;
+  const int64_t n = p.n;
+  const ProLayout Ly = pro_layout(K, m, F, k);
+  double* lut = reinterpret_cast<double*>(dsm + Ly.lut64);
+  float* lut32 = reinterpret_cast<float*>(dsm + Ly.lut32);
+  double* he = reinterpret_cast<double*>(dsm + Ly.he);
+  double* hf = reinterpret_cast<double*>(dsm + Ly.hf);
+  int32_t* hi = reinterpret_cast<int32_t*>(dsm + Ly.hi);
+  double* cf = reinterpret_cast<double*>(dsm + Ly.cf);
+  double* ce = reinterpret_cast<double*>(dsm + Ly.ce);
+  int32_t* cid = reinterpret_cast<int32_t*>(dsm + Ly.cid);
+  int32_t* wsum = reinterpret_cast<int32_t*>(dsm + Ly.ctrl);          // [8]
+  volatile float* hi_pub = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 64);
+  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctrl + 68);
+  const long long t0 = clock64();
+
+  // 1. float64 LUT -> smem, float32 copy of the fast books (prefilter)
+  const double* glut = p.lut64 + (size_t)q * K * m;
+  for (int i = tid; i < K * m; i += kProThreads) lut[i] = glut[i];
+  bool bad = false;
+  for (int i = tid; i < F * m; i += kProThreads) {
+    const int s = i / m, j = i - s * m;
+    const double x = glut[p.fast_books[s] * m + j];
+    // float32 certification needs finite entries with headroom; otherwise
+    // the query runs in float64 only ("wide" mode)
+    bad |= !(x <= 1.2676506002282294e30);  // 2^100 (also catches NaN)
+    lut32[i] = __double2float_rn(x);
+  }
+  const bool wide = __syncthreads_or(bad) != 0;
+
+  RCtx c;
+  c.lut = lut;
+  c.codes_full = p.codes_full;
+  c.fb = p.fast_books;
+  c.KP = p.KP; c.m = m; c.K = K; c.F = F;
+  c.sigma = p.sigma;
+  c.pw = n == 1;  // numpy row-sum order, see ref_row_sum
+  c.wide = wide;
+  c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
+
+  // 2. seeds: ids 0..k-1 scored exactly (search.py:141), sorted descending
+  //    by (exact, id) -> the sorted array is a valid max-heap.
+  constexpr int kSeedPer = 8;
+  double se[kSeedPer], sf[kSeedPer];
+  int32_t sr[kSeedPer];
+#pragma unroll
+  for (int r = 0; r < kSeedPer; ++r) {
+    const int i = tid + r * kProThreads;
+    if (i < k) {
+      const Row row = load_row(p.codes_full, p.KP, i);
+      se[r] = exact64(lut, m, K, c.pw, row);
+      sf[r] = fast64(lut, m, F, c.pw, p.fast_books, row);
+      he[i] = se[r];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSeedPer; ++r) {
+    const int i = tid + r * kProThreads;
+    if (i < k) {
+      int rank = 0;
+      for (int j = 0; j < k; ++j) rank += key_gt(he[j], j, se[r], i) ? 1 : 0;
+      sr[r] = rank;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSeedPer; ++r) {
+    const int i = tid + r * kProThreads;
+    if (i < k) {
+      he[sr[r]] = se[r];
+      hf[sr[r]] = sf[r];
+      hi[sr[r]] = i;
+    }
+  }
+  __syncthreads();
+
+  Live L;
+  L.refinements = L.insertions = L.candidates = L.certified = 0;
+  L.H.k = k;
+  L.H.reg = k <= 32 * kRegHeapRegs;
+  L.H.he = he;
+  L.H.hf = hf;
+  L.H.hi = hi;
+  double smin = 0.0;
+  if (warp == 0) {
+    L.H.load(lane);
+    live_update(L, F, p.sigma, wide);
+    smin = p.sigma == 0.0 ? 0.0 : smin_rd(lut, K, m, p.fast_books, F, lane);
+    const float h = stale_filter_hi(L, F, p.sigma, smin, wide, lane);
+    if (lane == 0) { *hi_pub = h; *flag = k < n ? 1 : 0; }
+  }
+  __syncthreads();
+
+  // 3. blocks of kProBlock items in database order
+  int64_t pos = k;
+  int64_t pro_cand = 0;
+  while (*flag) {
+    const int64_t base = (pos / kProBlock) * kProBlock;
+    const int64_t bend = min(n, base + kProBlock);
+    const float h = *hi_pub;
+    // 3a. fp32 prefilter of 8 consecutive items per thread (codes_fast rows)
+    const int64_t i0 = base + (int64_t)tid * 8;
+    uint32_t w[2 * FP];
+    {
+      const uint8_t* src = p.codes_fast + i0 * FP;
+      if (FP == 1) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+        w[0] = v.x; w[1] = v.y;
+      } else {
+#pragma unroll
+        for (int t = 0; t < FP / 2; ++t) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + t);
+          w[4 * t] = v.x; w[4 * t + 1] = v.y; w[4 * t + 2] = v.z; w[4 * t + 3] = v.w;
+        }
+      }
+    }
+    uint32_t mask = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float x = 0.f;
+#pragma unroll
+      for (int s = 0; s < FP; ++s) {
+        const int b = j * FP + s;
+        const uint32_t code = (w[b >> 2] >> ((b & 3) * 8)) & 0xffu;
+        if (s < F) x += lut32[s * m + code];
+      }
+      const int64_t i = i0 + j;
+      mask |= ((i >= pos) & (i < bend) & (wide | (x < h))) ? (1u << j) : 0u;
+    }
+    // 3b. ordered compaction (thread order = item order)
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = incl - cnt, ncand = 0;
+#pragma unroll
+    for (int t = 0; t < kProThreads / 32; ++t) {
+      const int v = wsum[t];
+      off += t < warp ? v : 0;
+      ncand += v;
+    }
+    while (mask) {
+      const int j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      cid[off++] = (int32_t)(i0 + j);
+    }
+    __syncthreads();
+    // 3c. float64 fast/exact scores of the prefiltered items (rows from L2/HBM)
+    {
+      Row rows[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int ci = tid + r * kProThreads;
+        if (ci < ncand) rows[r] = load_row(p.codes_full, p.KP, cid[ci]);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int ci = tid + r * kProThreads;
+        if (ci < ncand) {
+          cf[ci] = fast64(lut, m, F, c.pw, p.fast_books, rows[r]);
+          ce[ci] = exact64(lut, m, K, c.pw, rows[r]);
+        }
+      }
+    }
+    pro_cand += ncand;
+    __syncthreads();
+    // 3d. warp 0 applies search.py:148-154 in order, float64 compares only;
+    //     128-item windows: four 32-item sub-batches tested together, one
+    //     serial round per window up to its first insertion
+    if (warp == 0) {
+      constexpr int U = 4;
+      for (int w0 = 0; w0 < ncand; w0 += 32 * U) {
+        double f[U], e[U];
+        int32_t ids[U];
+        bool valid[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = w0 + u * 32 + lane;
+          valid[u] = i < ncand;
+          f[u] = valid[u] ? cf[i] : 0.0;
+          e[u] = valid[u] ? ce[i] : 0.0;
+          ids[u] = valid[u] ? cid[i] : 0;
+        }
+        uint32_t done[U] = {0, 0, 0, 0};
+        for (;;) {
+          uint32_t rm[U], im[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const bool refined = valid[u] && !((done[u] >> lane) & 1u) && (f[u] < L.thr64);
+            rm[u] = __ballot_sync(kFull, refined);
+            im[u] = __ballot_sync(kFull, refined && (e[u] < L.T64));
+          }
+          int uf = U;  // first sub-batch holding an insertion
+#pragma unroll
+          for (int u = U - 1; u >= 0; --u)
+            if (im[u]) uf = u;
+          int first = 31;
+          double ne = 0.0, nf = 0.0;
+          int32_t nid = 0;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            uint32_t dec = 0;
+            if (u < uf) dec = kFull;
+            if (u == uf) {
+              first = __ffs(im[u]) - 1;
+              dec = kFull >> (31 - first);
+              ne = __shfl_sync(kFull, e[u], first);
+              nf = __shfl_sync(kFull, f[u], first);
+              nid = __shfl_sync(kFull, ids[u], first);
+            }
+            L.refinements += __popc(rm[u] & dec);
+            if ((rm[u] & dec) >> lane & 1u) record_survivor(c.surv, ids[u]);
+            done[u] |= dec;
+          }
+          if (uf == U) break;
+          L.H.replace_max(ne, nid, nf, lane);
+          live_update64(L, p.sigma);
+          ++L.insertions;
+        }
+      }
+      live_update(L, F, p.sigma, wide);
+      const float hn = stale_filter_hi(L, F, p.sigma, smin, wide, lane);
+      const int64_t nb = bend - max(pos, base);
+      bool more = bend < n && bend < p.pro_max;
+      if (bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
+      if (lane == 0) { *hi_pub = hn; *flag = more ? 1 : 0; }
+    }
+    pos = bend;
+    __syncthreads();
+  }
+
+  // 4. hand the state to the filter / replay kernels
+  if (warp == 0) L.H.store(lane);
+  __syncthreads();
+  for (int i = tid; i < k; i += kProThreads) {
+    p.heap_e[(size_t)q * k + i] = he[i];
+    p.heap_f[(size_t)q * k + i] = hf[i];
+    p.heap_i[(size_t)q * k + i] = hi[i];
+  }
+  if (tid == 0) {
+    QState st;
+    st.P = pos;
+    st.refinements = L.refinements;
+    st.insertions = L.insertions;
+    st.pro_cand = pro_cand;
+    st.pro_cycles = clock64() - t0;
+    st.hi = *hi_pub;
+    st.wide = wide ? 1 : 0;
+    p.qs[q] = st;
+  }
+}
+
+// ==========================================================================
+// K3: filter (the streaming hot path)
+// ==========================================================================
+template <int FP>
+struct FGeo {
+  static constexpr int R = FP <= 4 ? 32 : (FP == 8 ? 16 : 8);  // replicas per entry
+  static constexpr int BPR = 64 / R;                             // book slots per 256-B row
+  static constexpr int P = (FP + BPR - 1) / BPR;                 // 64 KiB pages
+  static constexpr int IPC = 16 / FP;                            // items per 16-B chunk
+  static constexpr int V = 4;                                    // chunks per lane per tile
+  static constexpr int TILE = 32 * V * IPC;                      // items per warp tile
+  static constexpr uint32_t kSmemEnd = kPage * (1 + P);          // absolute end of the pages
+};
+constexpr int kPrefetchTiles = 8;  // L2 bulk-prefetch distance (tiles)
+
+template <int FP>
+__global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_constant__ PipeParams p) {
+  using G = FGeo<FP>;
+  constexpr int IPC = G::IPC, V = G::V, TILE = G::TILE;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // The lane-private pages sit at absolute 64 KiB boundaries; the planned
+  // layout assumes the dynamic window starts at kDynBase.
+  uint32_t dyn_size;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_size));
+  const uint32_t dbase = smem_addr(dsm);
+  if (dbase != kDynBase || dbase + dyn_size < G::kSmemEnd) {
+    if (tid == 0) atomicExch(p.error, 1);
+    return;
+  }
+  // page address template of fast book s for this lane: (page << 16) | lane offset;
+  // byte 1 (the codeword) is filled in by one byte_perm per lookup
+  uint32_t Lp[FP];
+#pragma unroll
+  for (int s = 0; s < FP; ++s)
+    Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
+            (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
+
+  const int K = p.K, m = p.m, F = p.F;
+  const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
+  const int64_t U = (int64_t)p.Q * p.NR;
+  int64_t u0, u1, ustep;
+  if (p.range_major) {  // all CTAs sweep the ranges together: codes reused in L2
+    u0 = blockIdx.x; u1 = U; ustep = gridDim.x;
+  } else {              // contiguous unit blocks: one query's LUT serves many units
+    u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1;
+  }
+  const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
+  int cur_q = -1;
+  for (int64_t u = u0; u < u1; u += ustep) {
+    const int q = p.range_major ? (int)(u % p.Q) : (int)(u / p.NR);
+    const int r = p.range_major ? (int)(u / p.Q) : (int)(u % p.NR);
+    const int64_t P = p.qs[q].P;
+    const float hi = p.qs[q].hi;
+    const int wide = p.qs[q].wide;
+    const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
+    int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+    if (P >= r_hi) {  // decided by the prologue
+      if (lane == 0) slice[0] = 0;
+      continue;
+    }
+    if (wide) {  // float64 only: the replay rescans these slices
+      if (lane == 0) slice[0] = -1;
+      continue;
+    }
+    if (q != cur_q) {
+      __syncthreads();  // every warp is done with the previous query's pages
+      const double* glut = p.lut64 + (size_t)q * K * m;
+      for (int i = tid; i < FP * m * G::R; i += kFW * 32) {
+        const int s = i / (m * G::R);
+        const int rem = i - s * (m * G::R);
+        const int j = rem / G::R;
+        const int rr = rem - j * G::R;
+        const float v = s < F ? __double2float_rn(glut[p.fast_books[s] * m + j]) : 0.f;
+        sts_f32(kPage * (1 + s / G::BPR) + j * 256 + (s % G::BPR) * 4 * G::R + rr * 4, v);
+      }
+      __syncthreads();
+      cur_q = q;
+    }
+    const int64_t w_lo = r_lo + warp * SW;
+    const int64_t w_hi = min(w_lo + SW, n);
+    const int64_t start = max(w_lo, P);
+    if (start >= w_hi) {
+      if (lane == 0) slice[0] = 0;
+      continue;
+    }
+    int cnt = 0, npages = 0, cur_page = 0;
+    bool overflow = false;
+    int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
+    uint4 a[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + t / IPC + v * 32 + lane);
+    for (; t < w_hi; t += TILE) {
+      uint4 x[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = a[v];
+      if (t + TILE < w_hi) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + (t + TILE) / IPC + v * 32 + lane);
+      }
+      if (lane == 0 && t + kPrefetchTiles * TILE < w_hi)
+        prefetch_l2_bulk(codes + (t + kPrefetchTiles * TILE) / IPC, TILE * FP);
+      float f[V][IPC];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+#pragma unroll
+        for (int j = 0; j < IPC; ++j) {
+          float acc[FP];
+#pragma unroll
+          for (int s = 0; s < FP; ++s) {
+            const int byte = j * FP + s;
+            const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
+            acc[s] = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
+          }
+#pragma unroll
+          for (int h = 1; h < FP; h *= 2)
+#pragma unroll
+            for (int s = 0; s + h < FP; s += 2 * h) acc[s] = acc[s] + acc[s + h];
+          f[v][j] = acc[0];
+        }
+      }
+      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int j = 0; j < IPC; ++j) {
+            const int64_t i = t + (int64_t)(v * 32 + lane) * IPC + j;
+            if (i < start || i >= w_hi) f[v][j] = kInf;
+          }
+      }
+      float lm = f[0][0];
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int j = 0; j < IPC; ++j) lm = fminf(lm, f[v][j]);
+      if (!__any_sync(kFull, lm < hi)) continue;
+      // ordered append (v, lane, j) into the slice's pages
+      uint32_t mk[V];
+      int excl[V], vbase[V];
+      int T = 0;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        uint32_t mm = 0;
+#pragma unroll
+        for (int j = 0; j < IPC; ++j) mm |= (f[v][j] < hi ? 1u : 0u) << j;
+        mk[v] = mm;
+        const int cc = __popc(mm);
+        int inc = cc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        excl[v] = inc - cc;
+        vbase[v] = T;
+        T += __shfl_sync(kFull, inc, 31);
+      }
+      const int need = (cnt + T + kPG - 1) / kPG - npages;
+      int base_pg = 0;
+      if (!overflow && need > 0) {
+        if (npages + need > kMaxPages) {
+          overflow = true;
+        } else {
+          if (lane == 0) base_pg = atomicAdd(p.pool_top, need);
+          base_pg = __shfl_sync(kFull, base_pg, 0);
+          if ((int64_t)base_pg + need > p.pool_pages) overflow = true;
+          else if (lane < need) slice[1 + npages + lane] = base_pg + lane;
+        }
+      }
+      if (!overflow) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          uint32_t mm = mk[v];
+          int g = cnt + vbase[v] + excl[v];
+          while (mm) {
+            const int j = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const int pi = g / kPG;
+            const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
+            float fj = f[v][0];
+#pragma unroll
+            for (int jj = 1; jj < IPC; ++jj)
+              if (jj == j) fj = f[v][jj];
+            const int64_t id = t + (int64_t)(v * 32 + lane) * IPC + j;
+            p.pool[(int64_t)pid * kPG + (g % kPG)] = make_uint2((uint32_t)id, __float_as_uint(fj));
+            ++g;
+          }
+        }
+        if (need > 0) {
+          npages += need;
+          cur_page = base_pg + need - 1;
+        }
+      }
+      cnt += T;
+    }
+    if (lane == 0) slice[0] = overflow ? -1 : cnt;
+  }
+}
+
+// ==========================================================================
+// K4: replay
+// ==========================================================================
+// Decide one window of up to kWU*32 items given in database order
+// (u-major, then lane): items whose float32 fast score can be under the live
+// bound are compacted (in order) and decided 32 at a time.  The live bound
+// (fast score of the heap maximum) may RISE after an insertion; then the
+// items after the inserted one are compacted again under the new bound.
+__device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
+                                              const int32_t (&ids)[kWU], const float (&fv)[kWU],
+                                              const bool (&valid)[kWU], int32_t* sid,
+                                              float* sfv, int32_t* sidx) {
+  int pos0 = 0;  // first undecided window position (u * 32 + lane)
+  const uint32_t lt = (1u << lane) - 1u;
+  for (;;) {
+    const float hc = L.hi;
+    uint32_t lm[kWU];
+    int base[kWU];
+    int tot = 0;
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) {
+      lm[u] = __ballot_sync(kFull, valid[u] && (u * 32 + lane >= pos0) && (c.wide || fv[u] < hc));
+      base[u] = tot;
+      tot += __popc(lm[u]);
+    }
+    if (tot == 0) return;
+#pragma unroll
+    for (int u = 0; u < kWU; ++u) {
+      if ((lm[u] >> lane) & 1u) {
+        const int pos = base[u] + __popc(lm[u] & lt);
+        sid[pos] = ids[u];
+        sfv[pos] = fv[u];
+        sidx[pos] = u * 32 + lane;
+      }
+    }
+    __syncwarp();
+    bool restart = false;
+    for (int b0 = 0; b0 < tot && !restart; b0 += 32) {
+      const int j = b0 + lane;
+      const bool v = j < tot;
+      const int32_t id = v ? sid[j] : 0;
+      const float f = v ? sfv[j] : kInf;
+      const int32_t wpos = v ? sidx[j] : 0;
+      bool have = false;
+      double f64 = 0.0, e64 = 0.0;
+      if (v && (c.wide || f < L.hi)) {
+        const Row r = load_row(c.codes_full, c.KP, id);
+        f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
+        e64 = exact64(c.lut, c.m, c.K, c.pw, r);
+        have = true;
+      }
+      uint32_t done = 0;
+      for (;;) {
+        const bool cand = v && !((done >> lane) & 1u) && (c.wide || f < L.hi);
+        const Decided d = decide_round(L, c, lane, cand, f, id, have, f64, e64);
+        done |= d.done;
+        if (d.first < 0) break;
+        if (L.hi > hc) {  // bound rose: re-compact everything after the insertion
+          pos0 = __shfl_sync(kFull, wpos, d.first) + 1;
+          restart = true;
+          break;
+        }
+      }
+    }
+    __syncwarp();
+    if (!restart) return;
+  }
+}
+
+template <int FP>
+__global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ PipeParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int lane = threadIdx.x;
+  const int q = blockIdx.x;
+  const int K = p.K, m = p.m, F = p.F, k = p.k;
+  const int64_t n = p.n;
+  const RepLayout Ly = rep_layout(K, m, F, k);
+  double* lut = reinterpret_cast<double*>(dsm + Ly.lut64);
+  float* lut32 = reinterpret_cast<float*>(dsm + Ly.lut32);
+  double* he = reinterpret_cast<double*>(dsm + Ly.he);
+  double* hf = reinterpret_cast<double*>(dsm + Ly.hf);
+  int32_t* hi = reinterpret_cast<int32_t*>(dsm + Ly.hi);
+  int32_t* sid = reinterpret_cast<int32_t*>(dsm + Ly.wid);
+  float* sfv = reinterpret_cast<float*>(dsm + Ly.wfv);
+  int32_t* sidx = reinterpret_cast<int32_t*>(dsm + Ly.widx);
+  const long long t0 = clock64();
+  const QState st = p.qs[q];
+  for (int i = lane; i < k; i += 32) {
+    he[i] = p.heap_e[(size_t)q * k + i];
+    hf[i] = p.heap_f[(size_t)q * k + i];
+    hi[i] = p.heap_i[(size_t)q * k + i];
+  }
+  Live L;
+  L.refinements = st.refinements;
+  L.insertions = st.insertions;
+  L.candidates = L.certified = 0;
+  L.H.k = k;
+  L.H.reg = k <= 32 * kRegHeapRegs;
+  L.H.he = he;
+  L.H.hf = hf;
+  L.H.hi = hi;
+  int64_t fallback_slices = 0, listed = 0;
+  if (st.P < n) {
+    const double* glut = p.lut64 + (size_t)q * K * m;
+    for (int i = lane; i < K * m; i += 32) lut[i] = glut[i];
+    for (int i = lane; i < F * m; i += 32) {
+      const int s = i / m, j = i - s * m;
+      lut32[i] = __double2float_rn(glut[p.fast_books[s] * m + j]);
+    }
+    __syncwarp();
+    L.H.load(lane);
+    const bool wide = st.wide != 0;
+    live_update(L, F, p.sigma, wide);
+    RCtx c;
+    c.lut = lut;
+    c.codes_full = p.codes_full;
+    c.fb = p.fast_books;
+    c.KP = p.KP; c.m = m; c.K = K; c.F = F;
+    c.sigma = p.sigma;
+    c.pw = false;  // n >= 2 here (P >= k >= 1 and P < n)
+    c.wide = wide;
+    c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
+    const int64_t SW = p.RS / kFW;
+    for (int r = 0; r < p.NR; ++r) {
+      for (int w = 0; w < kFW; ++w) {
+        const int64_t lo = max((int64_t)r * p.RS + w * SW, st.P);
+        const int64_t hi_ = min((int64_t)r * p.RS + (w + 1) * SW, n);
+        if (lo >= hi_) continue;
+        const int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + w) * kSliceInts;
+        const int cnt = slice[0];
+        if (cnt >= 0) {
+          listed += cnt;
+          for (int e0 = 0; e0 < cnt; e0 += kWU * 32) {
+            int32_t ids[kWU];
+            float fv[kWU];
+            bool valid[kWU];
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+              const int e = e0 + u * 32 + lane;
+              valid[u] = e < cnt;
+              uint2 ent = make_uint2(0, 0);
+              if (valid[u]) ent = p.pool[(int64_t)slice[1 + e / kPG] * kPG + (e % kPG)];
+              ids[u] = (int32_t)ent.x;
+              fv[u] = __uint_as_float(ent.y);
+            }
+            replay_window(L, c, lane, ids, fv, valid, sid, sfv, sidx);
+          }
+        } else {
+          // candidates overflowed the slice's pages: rescan its items from the codes
+          ++fallback_slices;
+          for (int64_t i0 = lo; i0 < hi_; i0 += kWU * 32) {
+            int32_t ids[kWU];
+            float fv[kWU];
+            bool valid[kWU];
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+              const int64_t i = i0 + u * 32 + lane;
+              valid[u] = i < hi_;
+              ids[u] = (int32_t)i;
+              float x = 0.f;
+              if (valid[u]) {
+                const Row r2 = load_row(p.codes_fast, FP, i);
+#pragma unroll
+                for (int s = 0; s < FP; ++s)
+                  if (s < F) x += lut32[s * m + (int)r2.byte(s)];
+              }
+              fv[u] = x;
+            }
+            replay_window(L, c, lane, ids, fv, valid, sid, sfv, sidx);
+          }
+        }
+      }
+    }
+    L.H.store(lane);
+  }
+  __syncwarp();
+  // output: heap ascending by (score, id) (search.py:156-165)
+  for (int i = lane; i < k; i += 32) {
+    const int src = k - 1 - i;
+    p.ids[(size_t)q * k + i] = hi[src];
+    p.scores[(size_t)q * k + i] = he[src];
+  }
+  if (lane == 0) {
+    if (p.refinements) p.refinements[q] = p.exact_mode ? n : L.refinements;
+    if (p.stats) {
+      int64_t* s = p.stats + (size_t)q * kStats;
+      s[0] = L.insertions;
+      s[1] = L.candidates;
+      s[2] = L.certified;
+      s[3] = st.P;
+      s[4] = st.pro_cycles;
+      s[5] = clock64() - t0;
+      s[6] = fallback_slices;
+      s[7] = st.wide;
+      s[8] = st.pro_cand;
+      s[9] = listed;
+      s[10] = st.insertions;
+      s[11] = __float_as_int(st.hi);
+      for (int j = 12; j < kStats; ++j) s[j] = 0;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// host launch
+// --------------------------------------------------------------------------
+template <int FP>
+cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s,
+                             cudaEvent_t* ev) {
+  using G = FGeo<FP>;
+  const ProLayout pl = pro_layout(p.K, p.m, p.F, p.k);
+  const RepLayout rl = rep_layout(p.K, p.m, p.F, p.k);
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(icq_prologue_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pl.total)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(icq_filter_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kSmemWindow - kDynBase))) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(icq_replay_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)rl.total)) != cudaSuccess)
+    return e;
+  if (ev) cudaEventRecord(ev[0], s);
+  icq_prologue_kernel<FP><<<p.Q, kProThreads, pl.total, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[1], s);
+  icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[2], s);
+  icq_replay_kernel<FP><<<p.Q, 32, rl.total, s>>>(p);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (ev) cudaEventRecord(ev[3], s);
+  return cudaSuccess;
+}
+
+}  // namespace icq

@@ -18,7 +18,26 @@ struct FastBooks {
   uint8_t b[kMaxK];
 };
 
-struct ScanParams {
+// Per-query state handed from the prologue to the filter and replay kernels.
+struct QState {
+  int64_t P;            // prologue end: items [0, P) are decided
+  int64_t refinements;  // refinements so far (search.py:150)
+  int64_t insertions;
+  int64_t pro_cand;     // items the prologue scored in float64
+  int64_t pro_cycles;
+  float hi;             // float32 candidate threshold of the filter (x32 < hi)
+  int32_t wide;         // float32 certification off: float64 only
+};
+
+constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
+constexpr int kPG = 128;         // candidate pool page (entries)
+constexpr int kMaxPages = 32;    // pages per slice (more -> the replay rescans the slice)
+constexpr int kSliceInts = 1 + kMaxPages;
+constexpr int kProThreads = 256;
+constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
+constexpr int64_t kRangeAlign = 32768;  // ranges / padding: whole filter tiles of every warp
+
+struct PipeParams {
   const uint8_t* codes_fast;  // [n_pad * FP]   fast books only (row-major), zero padded
   const uint8_t* codes_full;  // [n_pad * KP]   all books (row-major), zero padded
   const double* lut64;        // [Q][K][m]
@@ -28,32 +47,34 @@ struct ScanParams {
   uint32_t* survivors;        // [Q*words] or null
   int64_t* stats;             // [Q*kStats] or null
   int32_t* error;             // device error word
+  // workspace
+  QState* qs;                 // [Q]
+  double* heap_e;             // [Q*k]
+  double* heap_f;             // [Q*k]
+  int32_t* heap_i;            // [Q*k]
+  uint2* pool;                // [pool_pages * kPG] candidates {id, float32 fast bits}
+  int32_t* pool_top;          // pages handed out
+  int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
+  int64_t pool_pages;
   int64_t n;
-  int64_t nseg;
   int64_t words;              // survivors bitmap words per query
+  int64_t RS;                 // items per range (multiple of kRangeAlign)
   double sigma;
-  int32_t K, m, KP, F;
-  int32_t k;
+  int32_t Q, K, m, KP, F, k;
+  int32_t NR;                 // ranges per query
+  int32_t range_major;        // filter unit order (L2 reuse of codes larger than L2)
   int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
-  int32_t debug;              // experiments only (ICQ_DEBUG env): bit 0 = replay skips phase 2
-  int32_t nb;                 // slots in the ring
-  uint32_t off_lut64, off_heap_e, off_heap_f, off_heap_i, off_ctrl;
-  uint32_t off_slots;         // contiguous ring of nb slots (aliased by the prologue buffer)
-  uint32_t slot_bytes;
-  // sub-layout of one slot (byte offsets from the slot start): per-warp meta
-  // (candidate count, filter threshold used, warp minimum), then per-warp
-  // candidate lists (id, fast32, code row)
-  uint32_t so_lmin, so_eid, so_ef32, so_erow;  // so_lmin: per-lane minima (fallback gating)
-  int32_t cw;                 // candidate list capacity per scan warp per segment
-  int32_t dense_chunk;        // items per prologue chunk
-  uint32_t smem_end;          // absolute end of the planned layout
-  uint32_t dyn_bytes;
+  int32_t pro_div;            // prologue stops once a block's candidates <= items / pro_div
+  int64_t pro_min, pro_max;   // prologue length bounds (items)
   uint8_t fast_books[kMaxK];
 };
 
 bool make_lut_prog(int d, LutProg* out);
 cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, int m, int d,
                        int Q, const LutProg* prog_dev, cudaStream_t s);
-cudaError_t launch_scan(ScanParams& p, int FP, int Q, cudaStream_t s, int* unsupported);
+// prologue -> filter -> replay for one batch (icq_pipeline.cu)
+// ev: optional 4 events recorded before the prologue, filter, replay and after it
+cudaError_t launch_pipeline(const PipeParams& p, int FP, int filter_ctas, cudaStream_t s,
+                            int* unsupported, cudaEvent_t* ev = nullptr);
 
 }  // namespace icq

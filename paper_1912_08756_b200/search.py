@@ -28,13 +28,12 @@ from . import _native
 from .data import DeviceError, UnsupportedError, ValidationError
 
 
-# per-query int64 diagnostics written by the scan kernel (icq_b200.h stats_dev)
+# per-query int64 diagnostics written by the replay kernel (icq_b200.h stats_dev)
 STATS_FIELDS = 16
 STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
-               "prologue_cycles", "phase2_cycles", "replay_wait_cycles", "wide",
-               "prologue_score_cycles", "prologue_decide_cycles", "prologue_insert_cycles",
-               "fallback_segments", "phase2_segments", "replay_active_cycles",
-               "replay_fallback_cycles", "prologue_rounds")
+               "prologue_cycles", "replay_cycles", "rescanned_slices", "wide",
+               "prologue_f64_scored", "filter_candidates", "prologue_insertions",
+               "filter_hi_f32_bits", "reserved12", "reserved13", "reserved14", "reserved15")
 
 
 @dataclass

@@ -74,11 +74,28 @@ CONFIGS = [
     (7000, 20, 8, 256, 8, False),
     (4100, 6, 16, 64, 16, False),
     (20000, 32, 8, 256, 2, False),
+    (100000, 16, 16, 256, 4, False),
 ]
 
+# Pipeline shapes (icq_capi.cu planning knobs, read on every call):
+#   default   - the prologue decides small databases alone
+#   filter    - 2048-item prologue: the filter kernel + in-order replay of its slices
+#   overflow  - as filter, with a 2-page candidate pool: slices overflow and
+#               the replay rescans them from the codes
+#   subbatch  - as filter, queries in sub-batches of 4
+MODES = {
+    "default": {},
+    "filter": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"},
+    "overflow": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_POOL_PAGES": "2"},
+    "subbatch": {"ICQ_PRO_MAX": "4096", "ICQ_PRO_MIN": "0", "ICQ_QBATCH": "4"},
+}
 
+
+@pytest.mark.parametrize("mode", sorted(MODES))
 @pytest.mark.parametrize("cfg", CONFIGS)
-def test_random_vs_oracle_with_survivors(cfg):
+def test_random_vs_oracle_with_survivors(cfg, mode, monkeypatch):
+    for key, val in MODES[mode].items():
+        monkeypatch.setenv(key, val)
     n, d, K, m, F, dup = cfg
     rng = np.random.default_rng(n + d + K + m + F)
     books, codes, fast = _random_case(rng, n, d, K, m, F, dup)
@@ -159,8 +176,11 @@ def test_validation_errors():
                          np.array([0], dtype=np.uint32))
 
 
-def test_wide_mode_huge_values():
+@pytest.mark.parametrize("mode", sorted(MODES))
+def test_wide_mode_huge_values(mode, monkeypatch):
     """LUT entries beyond float32 headroom: float64-only path, still exact."""
+    for key, val in MODES[mode].items():
+        monkeypatch.setenv(key, val)
     rng = np.random.default_rng(11)
     books, codes, fast = _random_case(rng, 3000, 4, 4, 16, 2)
     books[0, 3] = 3e25
