@@ -346,11 +346,18 @@ def main():
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),
                     "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
                     "replay_cycles_per_query": float(stats[:, 5].mean().item()),
-                    "rescanned_slices": int(stats[:, 6].sum().item()),
+                    "rescanned_slices": int((stats[:, 6].long() & 0xFFFFF).sum().item()),
+                    "overflow_slices_pages": int(((stats[:, 6].long() >> 20) & 0xFFFFF).sum().item()),
+                    "overflow_slices_pool": int((stats[:, 6].long() >> 40).sum().item()),
                     "wide_queries": int(stats[:, 7].sum().item()),
                     "prologue_f64_scored_per_query": float(stats[:, 8].mean().item()),
                     "filter_candidates_per_query": float(stats[:, 9].mean().item()),
                     "filter_pass_fraction": float(stats[:, 9].mean().item() / w.n),
+                    "prologue_phase_cycles_per_query": {
+                        "prefilter": float(stats[:, 12].mean().item()),
+                        "score": float(stats[:, 13].mean().item()),
+                        "decide": float(stats[:, 14].mean().item()),
+                        "blocks": float(stats[:, 15].mean().item())},
                     "recall_vs_exact": recall},
         "roofline": {"bound": "hbm", "achieved": filter_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": filter_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),

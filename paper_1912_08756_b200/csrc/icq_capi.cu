@@ -355,7 +355,12 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     int64_t nr = (units + Qb - 1) / Qb;
     if (nr < 1) nr = 1;
     int64_t rs = (h->n + nr - 1) / nr;
-    if (big && rs > ((int64_t)4 << 20)) rs = (int64_t)4 << 20;
+    // slices (RS / 16 items) small enough that a loose threshold rarely
+    // overflows a slice's kMaxPages * kPG candidates
+    int64_t cap = h->n / 16;
+    if (cap < ((int64_t)1 << 18)) cap = (int64_t)1 << 18;
+    if (big) cap = (int64_t)4 << 20;
+    if (rs > cap) rs = cap;
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
@@ -368,8 +373,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
   }
   {
-    int64_t entries = (int64_t)Qb * h->n / 64;
-    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)128 << 20;
+    int64_t entries = (int64_t)Qb * h->n / 32;
+    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)256 << 20;
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
     p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
   }
@@ -387,7 +392,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t b_qs = al(sizeof(QState) * Qb);
   const size_t b_he = al((size_t)Qb * k * 8), b_hi = al((size_t)Qb * k * 4);
-  const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint2));
+  const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint4));
   const size_t b_top = 256;
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
   const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl;
@@ -399,7 +404,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.heap_e = reinterpret_cast<double*>(o); o += b_he;
     p.heap_f = reinterpret_cast<double*>(o); o += b_he;
     p.heap_i = reinterpret_cast<int32_t*>(o); o += b_hi;
-    p.pool = reinterpret_cast<uint2*>(o); o += b_pool;
+    p.pool = reinterpret_cast<uint4*>(o); o += b_pool;
     p.pool_top = reinterpret_cast<int32_t*>(o); o += b_top;
     p.slices = reinterpret_cast<int32_t*>(o);
   }

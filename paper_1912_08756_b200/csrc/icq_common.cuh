@@ -255,13 +255,19 @@ __device__ __forceinline__ void live_update(Live& L, int F, double sigma, bool w
 //              has fast < bound <= M), and bound <= M;
 //  sigma  > 0: U = max(M, T - Smin) never increases (inserted x: fast(x) <=
 //              exact(x) - Smin < T - Smin) and bound <= U; filter at U + sigma.
-// Returns the float32 value `hi` with x32 >= hi  =>  fast64 >= every future
-// bound + sigma, i.e. an item is a candidate iff x32 < hi.
-__device__ __forceinline__ float stale_filter_hi(const Live& L, int F, double sigma, double smin,
+// An item is a candidate iff fast64 < thr.  The float32 pre-test: x32 < lo
+// => candidate, x32 >= hi => not; in between (near-ties, and the exact ties
+// that few-codeword books produce in bulk) the caller sums fast64 exactly.
+struct StaleThr {
+  double thr;
+  float lo, hi;
+};
+__device__ __forceinline__ StaleThr stale_filter(const Live& L, int F, double sigma, double smin,
                                                  bool wide, int lane) {
-  if (wide) return kInf;
+  StaleThr r{__longlong_as_double(0x7ff0000000000000LL), kInf, kInf};
+  if (wide) return r;
   const double M = L.H.max_fast_all(lane);
-  if (L.H.any_nan_fast(lane)) return kInf;
+  if (L.H.any_nan_fast(lane)) return r;
   double thr;
   if (sigma == 0.0) {
     thr = M;
@@ -272,10 +278,10 @@ __device__ __forceinline__ float stale_filter_hi(const Live& L, int F, double si
     const double u = fmax(M, __dadd_ru(ts, fabs(L.T64) * 1e-12));
     thr = __dadd_ru(u, sigma);
   }
-  if (!(thr == thr)) return kInf;
-  float lo, hi;
-  certified_bounds(thr, F, lo, hi);
-  return hi;
+  if (!(thr == thr)) return r;
+  r.thr = thr;
+  certified_bounds(thr, F, r.lo, r.hi);
+  return r;
 }
 
 __device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {

@@ -9,7 +9,7 @@
 // The reference walks the database in order with a heap whose FAST score of
 // the maximum is the pruning bound (:149).  That chain is sequential, but the
 // bound is dominated by a monotone stale threshold (see
-// stale_filter_hi): once the heap has settled, one threshold is valid for
+// stale_filter): once the heap has settled, one threshold is valid for
 // every later item, so the streaming part can run on all SMs at once and
 // only the few items below it need the in-order replay.
 //
@@ -34,6 +34,8 @@
 // Every decision compares the reference's float64 values, so ids, scores,
 // refinement counts and survivor sets are bitwise the reference's.
 #pragma once
+#include <type_traits>
+
 #include "icq_common.cuh"
 
 namespace icq {
@@ -57,6 +59,33 @@ struct Decided {
   int first;      // inserting lane or -1
   uint32_t done;  // lanes decided in this round
 };
+
+// Fast-code tuple of item j of a 16-byte chunk (FP <= 8 bytes, little-endian
+// in .x/.y); runtime j selects words, no dynamically indexed arrays.
+template <int FP>
+__device__ __forceinline__ uint2 chunk_tuple(const uint4& xv, int j) {
+  if (FP <= 4) {
+    const int bo = j * FP;
+    const int wi = bo >> 2;
+    uint32_t w = ((wi == 0) ? xv.x : (wi == 1) ? xv.y : (wi == 2) ? xv.z : xv.w) >> ((bo & 3) * 8);
+    if (FP < 4) w &= (1u << (8 * FP)) - 1u;
+    return make_uint2(w, 0u);
+  }
+  return j == 0 ? make_uint2(xv.x, xv.y) : make_uint2(xv.z, xv.w);  // FP == 8
+}
+
+// float64 fast score of a tuple in the reference's order (search.py:94,
+// sequential in book order for n >= 2); lut64f holds the fast books' rows.
+template <int FP>
+__device__ __forceinline__ double tuple_f64(uint2 t, const double* lut64f, int m, int F) {
+  double d = 0.0;
+#pragma unroll
+  for (int s = 0; s < FP; ++s) {
+    const uint32_t w = s < 4 ? t.x : t.y;
+    if (s < F) d = __dadd_rn(d, lut64f[s * m + ((w >> (8 * (s & 3))) & 0xffu)]);
+  }
+  return d;
+}
 
 // One decision round over up to 32 items in database order (lane order):
 // search.py:149-154 applied until the first insertion.
@@ -135,19 +164,24 @@ __host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
 
 constexpr int kWU = 8;  // replay window: kWU x 32 entries
 struct RepLayout {
-  uint32_t lut64, lut32, he, hf, hi, wid, wfv, widx, total;
+  uint32_t lut64, lutf, he, hf, hi, wid, widx, wfv, meta, cum, ring, total;
 };
+constexpr int kSG = 64;    // slices whose meta the replay stages in shared memory at once
+constexpr int kCH = 1024;  // candidate entries per staged chunk (two chunks in flight)
 __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   RepLayout L;
   uint32_t o = 0;
   L.lut64 = o; o = al16(o + (uint32_t)K * m * 8);
-  L.lut32 = o; o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 4);
+  L.lutf = o;  o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 8);
   L.he = o;    o = al16(o + (uint32_t)k * 8);
   L.hf = o;    o = al16(o + (uint32_t)k * 8);
   L.hi = o;    o = al16(o + (uint32_t)k * 4);
   L.wid = o;   o = al16(o + kWU * 32 * 4);
-  L.wfv = o;   o = al16(o + kWU * 32 * 4);
+  L.wfv = o;   o = al16(o + kWU * 32 * 8);
   L.widx = o;  o = al16(o + kWU * 32 * 4);
+  L.meta = o;  o = al16(o + kSG * kSliceInts * 4);
+  L.cum = o;   o = al16(o + (kSG + 1) * 4);
+  L.ring = o;  o = al16(o + 2 * kCH * 16);
   L.total = o;
   return L;
 }
@@ -172,7 +206,7 @@ static __device__ double smin_rd(const double* lut, int K, int m, const uint8_t*
 // K2: prologue
 // ==========================================================================
 template <int FP>
-__global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_constant__ PipeParams p) {
+__global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __grid_constant__ PipeParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
@@ -188,8 +222,10 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
   double* ce = reinterpret_cast<double*>(dsm + Ly.ce);
   int32_t* cid = reinterpret_cast<int32_t*>(dsm + Ly.cid);
   int32_t* wsum = reinterpret_cast<int32_t*>(dsm + Ly.ctrl);          // [8]
-  volatile float* hi_pub = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 64);
-  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctrl + 68);
+  volatile float* pub_lo = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 64);
+  volatile float* pub_hi = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 68);
+  volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctrl + 72);
+  volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctrl + 80);
   const long long t0 = clock64();
 
   // 1. float64 LUT -> smem, float32 copy of the fast books (prefilter)
@@ -265,18 +301,23 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
     L.H.load(lane);
     live_update(L, F, p.sigma, wide);
     smin = p.sigma == 0.0 ? 0.0 : smin_rd(lut, K, m, p.fast_books, F, lane);
-    const float h = stale_filter_hi(L, F, p.sigma, smin, wide, lane);
-    if (lane == 0) { *hi_pub = h; *flag = k < n ? 1 : 0; }
+    const StaleThr t = stale_filter(L, F, p.sigma, smin, wide, lane);
+    if (lane == 0) { *pub_lo = t.lo; *pub_hi = t.hi; *pub_thr = t.thr; *flag = k < n ? 1 : 0; }
   }
   __syncthreads();
 
   // 3. blocks of kProBlock items in database order
   int64_t pos = k;
   int64_t pro_cand = 0;
+  long long tp[3] = {0, 0, 0};
+  int64_t nblocks = 0;
   while (*flag) {
+    const long long ta = clock64();
+    ++nblocks;
     const int64_t base = (pos / kProBlock) * kProBlock;
     const int64_t bend = min(n, base + kProBlock);
-    const float h = *hi_pub;
+    const float h = *pub_hi, hl = *pub_lo;
+    const double hthr = *pub_thr;
     // 3a. fp32 prefilter of 8 consecutive items per thread (codes_fast rows)
     const int64_t i0 = base + (int64_t)tid * 8;
     uint32_t w[2 * FP];
@@ -304,7 +345,18 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
         if (s < F) x += lut32[s * m + code];
       }
       const int64_t i = i0 + j;
-      mask |= ((i >= pos) & (i < bend) & (wide | (x < h))) ? (1u << j) : 0u;
+      bool cand = wide || x < hl;
+      if (!cand && x < h) {  // float32 cannot decide: exact float64 fast score
+        double d = 0.0;
+#pragma unroll
+        for (int s = 0; s < FP; ++s) {
+          const int b = j * FP + s;
+          const uint32_t code = (w[b >> 2] >> ((b & 3) * 8)) & 0xffu;
+          if (s < F) d = __dadd_rn(d, lut[p.fast_books[s] * m + code]);
+        }
+        cand = d < hthr;
+      }
+      mask |= ((i >= pos) & (i < bend) & cand) ? (1u << j) : 0u;
     }
     // 3b. ordered compaction (thread order = item order)
     const int cnt = __popc(mask);
@@ -329,6 +381,7 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
       cid[off++] = (int32_t)(i0 + j);
     }
     __syncthreads();
+    const long long tb = clock64();
     // 3c. float64 fast/exact scores of the prefiltered items (rows from L2/HBM)
     {
       Row rows[8];
@@ -348,6 +401,7 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
     }
     pro_cand += ncand;
     __syncthreads();
+    const long long tc = clock64();
     // 3d. warp 0 applies search.py:148-154 in order, float64 compares only;
     //     128-item windows: four 32-item sub-batches tested together, one
     //     serial round per window up to its first insertion
@@ -403,19 +457,38 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
         }
       }
       live_update(L, F, p.sigma, wide);
-      const float hn = stale_filter_hi(L, F, p.sigma, smin, wide, lane);
+      const StaleThr tn = stale_filter(L, F, p.sigma, smin, wide, lane);
       const int64_t nb = bend - max(pos, base);
       bool more = bend < n && bend < p.pro_max;
       if (bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
-      if (lane == 0) { *hi_pub = hn; *flag = more ? 1 : 0; }
+      if (lane == 0) { *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *flag = more ? 1 : 0; }
     }
     pos = bend;
     __syncthreads();
+    tp[0] += tb - ta;
+    tp[1] += tc - tb;
+    tp[2] += clock64() - tc;
   }
 
   // 4. hand the state to the filter / replay kernels
   if (warp == 0) L.H.store(lane);
   __syncthreads();
+  if (tid == 0) {
+    // sigma == 0: thr = M is the fast score of a heap item; every item with
+    // its fast-code tuple ties at thr exactly (never a candidate)
+    int best = -1;
+    for (int i = 0; i < k; ++i)
+      if (best < 0 || hf[i] > hf[best]) best = i;
+    uint2 tup = make_uint2(0u, 0u);
+    const bool ok = p.sigma == 0.0 && !wide && FP <= 8 && best >= 0 && hf[best] == *pub_thr;
+    if (ok) {
+      const Row r = load_row(p.codes_fast, FP, hi[best]);
+      tup = make_uint2(r.w[0], r.w[1]);
+    }
+    wsum[0] = (int32_t)tup.x;
+    wsum[1] = (int32_t)tup.y;
+    wsum[2] = ok ? 1 : 0;
+  }
   for (int i = tid; i < k; i += kProThreads) {
     p.heap_e[(size_t)q * k + i] = he[i];
     p.heap_f[(size_t)q * k + i] = hf[i];
@@ -428,8 +501,19 @@ __global__ void __launch_bounds__(kProThreads) icq_prologue_kernel(const __grid_
     st.insertions = L.insertions;
     st.pro_cand = pro_cand;
     st.pro_cycles = clock64() - t0;
-    st.hi = *hi_pub;
+    st.pro_t[0] = tp[0];
+    st.pro_t[1] = tp[1];
+    st.pro_t[2] = tp[2];
+    st.pro_t[3] = nblocks;
+    st.hi = *pub_hi;
+    st.lo = *pub_lo;
+    st.thr = *pub_thr;
+    st.mtup[0] = (uint32_t)wsum[0];
+    st.mtup[1] = (uint32_t)wsum[1];
+    st.mt_valid = wsum[2];
     st.wide = wide ? 1 : 0;
+    st.ovf_pages = 0;
+    st.ovf_pool = 0;
     p.qs[q] = st;
   }
 }
@@ -482,12 +566,16 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1;
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
+  double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
   int cur_q = -1;
   for (int64_t u = u0; u < u1; u += ustep) {
     const int q = p.range_major ? (int)(u % p.Q) : (int)(u / p.NR);
     const int r = p.range_major ? (int)(u / p.Q) : (int)(u % p.NR);
     const int64_t P = p.qs[q].P;
-    const float hi = p.qs[q].hi;
+    const float hi = p.qs[q].hi, lo = p.qs[q].lo;
+    const double thr = p.qs[q].thr;
+    const uint2 mtup = make_uint2(p.qs[q].mtup[0], p.qs[q].mtup[1]);
+    const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
@@ -510,6 +598,10 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         const float v = s < F ? __double2float_rn(glut[p.fast_books[s] * m + j]) : 0.f;
         sts_f32(kPage * (1 + s / G::BPR) + j * 256 + (s % G::BPR) * 4 * G::R + rr * 4, v);
       }
+      for (int i = tid; i < F * m; i += kFW * 32) {  // float64 fast tables (near-ties)
+        const int s = i / m, j = i - s * m;
+        lut64f[i] = glut[p.fast_books[s] * m + j];
+      }
       __syncthreads();
       cur_q = q;
     }
@@ -522,6 +614,20 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     }
     int cnt = 0, npages = 0, cur_page = 0;
     bool overflow = false;
+    // exact float64 fast score of item j of a code chunk, reference order
+    auto fast_f64 = [&](const uint4& xv, int j) -> double {
+      if constexpr (FP <= 8) {
+        return tuple_f64<FP>(chunk_tuple<FP>(xv, j), lut64f, m, F);
+      } else {
+        const uint32_t wd[4] = {xv.x, xv.y, xv.z, xv.w};
+        double d = 0.0;
+#pragma unroll
+        for (int s = 0; s < FP; ++s)
+          if (s < F) d = __dadd_rn(d, lut64f[s * m + ((wd[s >> 2] >> (8 * (s & 3))) & 0xffu)]);
+        return d;
+      }
+    };
+    using Mask = typename std::conditional<(V * IPC > 32), unsigned long long, uint32_t>::type;
     int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
     uint4 a[V];
 #pragma unroll
@@ -536,6 +642,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       }
       if (lane == 0 && t + kPrefetchTiles * TILE < w_hi)
         prefetch_l2_bulk(codes + (t + kPrefetchTiles * TILE) / IPC, TILE * FP);
+      // one warp tile: 32 lanes x V 16-byte chunks, items (v, lane, j)
       float f[V][IPC];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -556,72 +663,116 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           f[v][j] = acc[0];
         }
       }
-      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-#pragma unroll
-          for (int j = 0; j < IPC; ++j) {
-            const int64_t i = t + (int64_t)(v * 32 + lane) * IPC + j;
-            if (i < start || i >= w_hi) f[v][j] = kInf;
-          }
-      }
-      float lm = f[0][0];
+      // candidate bits (bit v*IPC + j): x32 < hi; band: not surely (x32 >= lo)
+      Mask cm = 0, bm = 0;
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int j = 0; j < IPC; ++j) lm = fminf(lm, f[v][j]);
-      if (!__any_sync(kFull, lm < hi)) continue;
-      // ordered append (v, lane, j) into the slice's pages
-      uint32_t mk[V];
-      int excl[V], vbase[V];
-      int T = 0;
+        for (int j = 0; j < IPC; ++j) {
+          cm |= (Mask)(f[v][j] < hi ? 1u : 0u) << (v * IPC + j);
+          bm |= (Mask)(f[v][j] >= lo ? 1u : 0u) << (v * IPC + j);
+        }
+      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
+#pragma unroll 1
+        for (int idx = 0; idx < V * IPC; ++idx) {
+          const int64_t i = t + (int64_t)((idx / IPC) * 32 + lane) * IPC + (idx % IPC);
+          if (i < start || i >= w_hi) cm &= ~((Mask)1 << idx);
+        }
+      }
+      if (!__any_sync(kFull, cm != 0)) continue;
+      // ---- slow path (most tiles hold a candidate or two): compact loops ----
+      auto xsel = [&](int v) {
+        uint4 r = x[0];
+#pragma unroll
+        for (int vv = 1; vv < V; ++vv)
+          if (v == vv) r = x[vv];
+        return r;
+      };
+      // near / exact ties with thr: exact float64 decides (tuple of the
+      // threshold item: fast == thr exactly, never a candidate)
+      bm &= cm;
+      while (bm) {
+        const int idx = (int)__ffsll((unsigned long long)bm) - 1;
+        bm &= bm - 1;
+        const uint4 xv = xsel(idx / IPC);
+        const int j = idx % IPC;
+        bool tie = false;
+        if constexpr (FP <= 8) {
+          const uint2 tj = chunk_tuple<FP>(xv, j);
+          tie = mt_valid && tj.x == mtup.x && tj.y == mtup.y;
+        }
+        if (tie || !(fast_f64(xv, j) < thr)) cm &= ~((Mask)1 << idx);
+      }
+      // per-v counts packed in 16-bit fields -> exclusive prefix over lanes
+      uint32_t cA = 0, cB = 0;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        uint32_t mm = 0;
-#pragma unroll
-        for (int j = 0; j < IPC; ++j) mm |= (f[v][j] < hi ? 1u : 0u) << j;
-        mk[v] = mm;
-        const int cc = __popc(mm);
-        int inc = cc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(kFull, inc, o);
-          if (lane >= o) inc += y;
-        }
-        excl[v] = inc - cc;
-        vbase[v] = T;
-        T += __shfl_sync(kFull, inc, 31);
+        const uint32_t cc = (uint32_t)__popcll((unsigned long long)((cm >> (v * IPC)) &
+                                                                    (((Mask)1 << IPC) - 1)));
+        if (v < 2) cA |= cc << (16 * v);
+        else cB |= cc << (16 * (v - 2));
       }
+      uint32_t iA = cA, iB = cB;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yA = __shfl_up_sync(kFull, iA, o);
+        const uint32_t yB = __shfl_up_sync(kFull, iB, o);
+        if (lane >= o) { iA += yA; iB += yB; }
+      }
+      const uint32_t tA = __shfl_sync(kFull, iA, 31), tB = __shfl_sync(kFull, iB, 31);
+      const int T = (int)((tA & 0xffffu) + (tA >> 16) + (tB & 0xffffu) + (tB >> 16));
+      if (T == 0) continue;
       const int need = (cnt + T + kPG - 1) / kPG - npages;
       int base_pg = 0;
       if (!overflow && need > 0) {
         if (npages + need > kMaxPages) {
           overflow = true;
+          if (lane == 0) atomicAdd(&p.qs[q].ovf_pages, 1);
         } else {
           if (lane == 0) base_pg = atomicAdd(p.pool_top, need);
           base_pg = __shfl_sync(kFull, base_pg, 0);
-          if ((int64_t)base_pg + need > p.pool_pages) overflow = true;
-          else if (lane < need) slice[1 + npages + lane] = base_pg + lane;
+          if ((int64_t)base_pg + need > p.pool_pages) {
+            overflow = true;
+            if (lane == 0) atomicAdd(&p.qs[q].ovf_pool, 1);
+          } else if (lane < need) {
+            slice[1 + npages + lane] = base_pg + lane;
+          }
         }
       }
       if (!overflow) {
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          uint32_t mm = mk[v];
-          int g = cnt + vbase[v] + excl[v];
-          while (mm) {
-            const int j = __ffs(mm) - 1;
-            mm &= mm - 1;
-            const int pi = g / kPG;
-            const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
-            float fj = f[v][0];
-#pragma unroll
-            for (int jj = 1; jj < IPC; ++jj)
-              if (jj == j) fj = f[v][jj];
-            const int64_t id = t + (int64_t)(v * 32 + lane) * IPC + j;
-            p.pool[(int64_t)pid * kPG + (g % kPG)] = make_uint2((uint32_t)id, __float_as_uint(fj));
-            ++g;
+        // every lane writes its own entries at its prefix position
+        const uint32_t eA = iA - cA, eB = iB - cB;
+        int curv = -1, g = 0;
+        while (cm) {
+          const int idx = (int)__ffsll((unsigned long long)cm) - 1;
+          cm &= cm - 1;
+          const int v = idx / IPC, j = idx % IPC;
+          if (v != curv) {  // first entry of chunk v: its position
+            curv = v;
+            const uint32_t tb = (v < 2 ? 0u : ((tA & 0xffffu) + (tA >> 16))) +
+                                (v & 1 ? ((v < 2 ? tA : tB) & 0xffffu) : 0u);
+            g = cnt + (int)tb + (int)(((v < 2 ? eA : eB) >> (16 * (v & 1))) & 0xffffu);
           }
+          float fj = f[0][0];
+#pragma unroll
+          for (int vv = 0; vv < V; ++vv)
+#pragma unroll
+            for (int jj = 0; jj < IPC; ++jj)
+              if (vv * IPC + jj == idx) fj = f[vv][jj];
+          const uint4 xv = xsel(v);
+          uint2 tail;
+          if constexpr (FP <= 8) {
+            tail = chunk_tuple<FP>(xv, j);
+          } else {
+            const unsigned long long db = (unsigned long long)__double_as_longlong(fast_f64(xv, j));
+            tail = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+          }
+          const int pi = g / kPG;
+          const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
+          const int64_t id = t + (int64_t)(v * 32 + lane) * IPC + j;
+          p.pool[(int64_t)pid * kPG + (g % kPG)] =
+              make_uint4((uint32_t)id, __float_as_uint(fj), tail.x, tail.y);
+          ++g;
         }
         if (need > 0) {
           npages += need;
@@ -637,25 +788,45 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
 // ==========================================================================
 // K4: replay
 // ==========================================================================
-// Decide one window of up to kWU*32 items given in database order
-// (u-major, then lane): items whose float32 fast score can be under the live
-// bound are compacted (in order) and decided 32 at a time.  The live bound
-// (fast score of the heap maximum) may RISE after an insertion; then the
-// items after the inserted one are compacted again under the new bound.
+// float64 fast score of a candidate entry: from its fast-code tuple
+// (FP <= 8) or stored directly (FP = 16)
+template <int FP>
+__device__ __forceinline__ double entry_f64(uint2 tail, const double* lutf, int m, int F) {
+  if constexpr (FP <= 8) return tuple_f64<FP>(tail, lutf, m, F);
+  else return __longlong_as_double((long long)(((unsigned long long)tail.y << 32) | tail.x));
+}
+
+// Decide one window of up to kWU*32 items in database order (u-major, then
+// lane), each with its float32 fast score and tuple.  Refined items (fast <
+// bound + sigma, search.py:149: certified float32 test, exact float64 from
+// the tuple in the uncertain band) are compacted in order, their exact
+// scores computed 32 at a time, and the first one under the heap maximum is
+// inserted (search.py:152-154).  An insertion moves the bound (up or down):
+// when it rises, the items after the insertion are compacted again.
+template <int FP>
 __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
-                                              const int32_t (&ids)[kWU], const float (&fv)[kWU],
-                                              const bool (&valid)[kWU], int32_t* sid,
-                                              float* sfv, int32_t* sidx) {
+                                              const int32_t (&ids)[kWU], const float (&f32)[kWU],
+                                              const uint2 (&tail)[kWU], const bool (&valid)[kWU],
+                                              int32_t* sid, int32_t* sidx, double* sfv,
+                                              const double* lutf) {
   int pos0 = 0;  // first undecided window position (u * 32 + lane)
   const uint32_t lt = (1u << lane) - 1u;
   for (;;) {
-    const float hc = L.hi;
+    const double thr = L.thr64;
+    const float hhi = L.hi;
     uint32_t lm[kWU];
+    double d[kWU];
     int base[kWU];
     int tot = 0;
 #pragma unroll
     for (int u = 0; u < kWU; ++u) {
-      lm[u] = __ballot_sync(kFull, valid[u] && (u * 32 + lane >= pos0) && (c.wide || fv[u] < hc));
+      bool cand = valid[u] && (u * 32 + lane >= pos0) && f32[u] < hhi;
+      d[u] = 0.0;
+      if (cand) {
+        d[u] = entry_f64<FP>(tail[u], lutf, c.m, c.F);
+        cand = d[u] < thr;
+      }
+      lm[u] = __ballot_sync(kFull, cand);
       base[u] = tot;
       tot += __popc(lm[u]);
     }
@@ -665,8 +836,8 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
       if ((lm[u] >> lane) & 1u) {
         const int pos = base[u] + __popc(lm[u] & lt);
         sid[pos] = ids[u];
-        sfv[pos] = fv[u];
         sidx[pos] = u * 32 + lane;
+        sfv[pos] = d[u];
       }
     }
     __syncwarp();
@@ -675,24 +846,31 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
       const int j = b0 + lane;
       const bool v = j < tot;
       const int32_t id = v ? sid[j] : 0;
-      const float f = v ? sfv[j] : kInf;
       const int32_t wpos = v ? sidx[j] : 0;
-      bool have = false;
-      double f64 = 0.0, e64 = 0.0;
-      if (v && (c.wide || f < L.hi)) {
-        const Row r = load_row(c.codes_full, c.KP, id);
-        f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
-        e64 = exact64(c.lut, c.m, c.K, c.pw, r);
-        have = true;
-      }
+      const double f64 = v ? sfv[j] : 0.0;
+      double e64 = 0.0;
+      if (v) e64 = exact64(c.lut, c.m, c.K, c.pw, load_row(c.codes_full, c.KP, id));
       uint32_t done = 0;
       for (;;) {
-        const bool cand = v && !((done >> lane) & 1u) && (c.wide || f < L.hi);
-        const Decided d = decide_round(L, c, lane, cand, f, id, have, f64, e64);
-        done |= d.done;
-        if (d.first < 0) break;
-        if (L.hi > hc) {  // bound rose: re-compact everything after the insertion
-          pos0 = __shfl_sync(kFull, wpos, d.first) + 1;
+        const bool refined = v && !((done >> lane) & 1u) && (f64 < L.thr64);
+        const bool ins = refined && (e64 < L.T64);
+        const uint32_t rmask = __ballot_sync(kFull, refined);
+        const uint32_t imask = __ballot_sync(kFull, ins);
+        const int first = imask ? __ffs(imask) - 1 : 31;
+        const uint32_t decided = imask ? (kFull >> (31 - first)) : kFull;
+        L.refinements += __popc(rmask & decided);
+        L.candidates += __popc(rmask & decided);
+        if (refined && ((decided >> lane) & 1u)) record_survivor(c.surv, id);
+        done |= decided;
+        if (!imask) break;
+        const double ne = __shfl_sync(kFull, e64, first);
+        const double nf = __shfl_sync(kFull, f64, first);
+        const int32_t nid = __shfl_sync(kFull, id, first);
+        L.H.replace_max(ne, nid, nf, lane);
+        live_update(L, c.F, c.sigma, false);
+        ++L.insertions;
+        if (L.thr64 > thr) {  // bound rose: re-compact everything after the insertion
+          pos0 = __shfl_sync(kFull, wpos, first) + 1;
           restart = true;
           break;
         }
@@ -712,13 +890,16 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
   const int64_t n = p.n;
   const RepLayout Ly = rep_layout(K, m, F, k);
   double* lut = reinterpret_cast<double*>(dsm + Ly.lut64);
-  float* lut32 = reinterpret_cast<float*>(dsm + Ly.lut32);
   double* he = reinterpret_cast<double*>(dsm + Ly.he);
   double* hf = reinterpret_cast<double*>(dsm + Ly.hf);
   int32_t* hi = reinterpret_cast<int32_t*>(dsm + Ly.hi);
   int32_t* sid = reinterpret_cast<int32_t*>(dsm + Ly.wid);
-  float* sfv = reinterpret_cast<float*>(dsm + Ly.wfv);
   int32_t* sidx = reinterpret_cast<int32_t*>(dsm + Ly.widx);
+  double* sfv = reinterpret_cast<double*>(dsm + Ly.wfv);
+  double* lutf = reinterpret_cast<double*>(dsm + Ly.lutf);
+  int32_t* smeta = reinterpret_cast<int32_t*>(dsm + Ly.meta);
+  int32_t* scum = reinterpret_cast<int32_t*>(dsm + Ly.cum);
+  uint4* ring = reinterpret_cast<uint4*>(dsm + Ly.ring);
   const long long t0 = clock64();
   const QState st = p.qs[q];
   for (int i = lane; i < k; i += 32) {
@@ -741,12 +922,11 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
     for (int i = lane; i < K * m; i += 32) lut[i] = glut[i];
     for (int i = lane; i < F * m; i += 32) {
       const int s = i / m, j = i - s * m;
-      lut32[i] = __double2float_rn(glut[p.fast_books[s] * m + j]);
+      lutf[i] = glut[p.fast_books[s] * m + j];
     }
     __syncwarp();
     L.H.load(lane);
-    const bool wide = st.wide != 0;
-    live_update(L, F, p.sigma, wide);
+    live_update(L, F, p.sigma, false);
     RCtx c;
     c.lut = lut;
     c.codes_full = p.codes_full;
@@ -754,58 +934,141 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
     c.KP = p.KP; c.m = m; c.K = K; c.F = F;
     c.sigma = p.sigma;
     c.pw = false;  // n >= 2 here (P >= k >= 1 and P < n)
-    c.wide = wide;
+    c.wide = false;
     c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
     const int64_t SW = p.RS / kFW;
-    for (int r = 0; r < p.NR; ++r) {
-      for (int w = 0; w < kFW; ++w) {
-        const int64_t lo = max((int64_t)r * p.RS + w * SW, st.P);
-        const int64_t hi_ = min((int64_t)r * p.RS + (w + 1) * SW, n);
-        if (lo >= hi_) continue;
-        const int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + w) * kSliceInts;
-        const int cnt = slice[0];
-        if (cnt >= 0) {
-          listed += cnt;
-          for (int e0 = 0; e0 < cnt; e0 += kWU * 32) {
-            int32_t ids[kWU];
-            float fv[kWU];
-            bool valid[kWU];
-#pragma unroll
-            for (int u = 0; u < kWU; ++u) {
-              const int e = e0 + u * 32 + lane;
-              valid[u] = e < cnt;
-              uint2 ent = make_uint2(0, 0);
-              if (valid[u]) ent = p.pool[(int64_t)slice[1 + e / kPG] * kPG + (e % kPG)];
-              ids[u] = (int32_t)ent.x;
-              fv[u] = __uint_as_float(ent.y);
-            }
-            replay_window(L, c, lane, ids, fv, valid, sid, sfv, sidx);
-          }
-        } else {
+    const int NS = p.NR * kFW;  // slices of this query, in database order
+    const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
+    for (int g0 = 0; g0 < NS; g0 += kSG) {
+      const int ng = min(kSG, NS - g0);
+      // group meta (counts + page ids) -> shared memory, all copies in flight at once
+      {
+        const int chunks = ng * kSliceInts / 4;  // 16-byte pieces
+        const uint4* src = reinterpret_cast<const uint4*>(qsl + (int64_t)g0 * kSliceInts);
+        for (int i = lane; i < chunks; i += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smeta + 4 * i)),
+                       "l"(src + i)
+                       : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+      }
+      int si = 0;
+      while (si < ng) {
+        const int cnt0 = smeta[si * kSliceInts];
+        if (cnt0 == 0) { ++si; continue; }
+        if (cnt0 < 0) {
           // candidates overflowed the slice's pages: rescan its items from the codes
-          ++fallback_slices;
+          int32_t ids2[kWU];
+          float f2[kWU];
+          uint2 t2[kWU];
+          bool valid2[kWU];
+          const int64_t j = g0 + si;
+          const int64_t lo = max(j * SW, st.P), hi_ = min((j + 1) * SW, n);
+          if (lo < hi_) ++fallback_slices;
           for (int64_t i0 = lo; i0 < hi_; i0 += kWU * 32) {
-            int32_t ids[kWU];
-            float fv[kWU];
-            bool valid[kWU];
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
               const int64_t i = i0 + u * 32 + lane;
-              valid[u] = i < hi_;
-              ids[u] = (int32_t)i;
-              float x = 0.f;
-              if (valid[u]) {
+              valid2[u] = i < hi_;
+              ids2[u] = (int32_t)i;
+              f2[u] = -kInf;  // no float32 score: the exact float64 one decides
+              t2[u] = make_uint2(0u, 0u);
+              if (valid2[u]) {
                 const Row r2 = load_row(p.codes_fast, FP, i);
+                if constexpr (FP <= 8) {
+                  t2[u] = make_uint2(r2.w[0], r2.w[1]);
+                } else {
+                  double x = 0.0;  // float64 fast score in the reference's order
 #pragma unroll
-                for (int s = 0; s < FP; ++s)
-                  if (s < F) x += lut32[s * m + (int)r2.byte(s)];
+                  for (int s2 = 0; s2 < FP; ++s2)
+                    if (s2 < F) x = __dadd_rn(x, lutf[s2 * m + (int)r2.byte(s2)]);
+                  const unsigned long long db = (unsigned long long)__double_as_longlong(x);
+                  t2[u] = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+                }
               }
-              fv[u] = x;
             }
-            replay_window(L, c, lane, ids, fv, valid, sid, sfv, sidx);
+            replay_window<FP>(L, c, lane, ids2, f2, t2, valid2, sid, sidx, sfv, lutf);
           }
+          ++si;
+          continue;
         }
+        // a run of listed slices [si, se): one virtual list, staged through
+        // the shared-memory ring in chunks of kCH entries (two in flight)
+        int se = si;
+        while (se < ng && smeta[se * kSliceInts] >= 0) ++se;
+        if (lane == 0) {
+          int acc = 0;
+          for (int t2 = si; t2 < se; ++t2) { scum[t2 - si] = acc; acc += smeta[t2 * kSliceInts]; }
+          scum[se - si] = acc;
+        }
+        __syncwarp();
+        const int ns = se - si;
+        const int total = scum[ns];
+        listed += total;
+        const int nch = (total + kCH - 1) / kCH;
+        auto issue_chunk = [&](int ch) {
+          uint4* dst = ring + (ch & 1) * kCH;
+          const int v0 = ch * kCH;
+          const int len = min(kCH, total - v0);
+          for (int i = lane; i < len; i += 32) {
+            const int v = v0 + i;
+            int lo2 = 0, hi2 = ns;  // slice t with scum[t] <= v < scum[t + 1]
+            while (hi2 - lo2 > 1) {
+              const int mid = (lo2 + hi2) >> 1;
+              if (scum[mid] <= v) lo2 = mid; else hi2 = mid;
+            }
+            const int e = v - scum[lo2];
+            const int32_t* sm = smeta + (si + lo2) * kSliceInts;
+            const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
+                         "l"(src)
+                         : "memory");
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        auto prefetch_rows = [&](int ch) {  // rows of the entries refined under the current bound
+          const uint4* src = ring + (ch & 1) * kCH;
+          const int len = min(kCH, total - ch * kCH);
+          for (int i = lane; i < len; i += 32) {
+            const uint4 ent = src[i];
+            if (__uint_as_float(ent.y) < L.hi)
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.codes_full + (int64_t)ent.x * p.KP));
+          }
+        };
+        issue_chunk(0);
+        if (nch > 1) issue_chunk(1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        prefetch_rows(0);
+        for (int ch = 0; ch < nch; ++ch) {
+          // chunk ch+1 lands first: its rows are prefetched one chunk ahead
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+          __syncwarp();
+          if (ch + 1 < nch) prefetch_rows(ch + 1);
+          const uint4* src = ring + (ch & 1) * kCH;
+          const int len = min(kCH, total - ch * kCH);
+          for (int w0 = 0; w0 < len; w0 += kWU * 32) {
+            int32_t ids[kWU];
+            float fv[kWU];
+            uint2 tl[kWU];
+            bool valid[kWU];
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+              const int e = w0 + u * 32 + lane;
+              valid[u] = e < len;
+              const uint4 ent = valid[u] ? src[e] : make_uint4(0, 0, 0, 0);
+              ids[u] = (int32_t)ent.x;
+              fv[u] = __uint_as_float(ent.y);
+              tl[u] = make_uint2(ent.z, ent.w);
+            }
+            replay_window<FP>(L, c, lane, ids, fv, tl, valid, sid, sidx, sfv, lutf);
+          }
+          __syncwarp();
+          if (ch + 2 < nch) issue_chunk(ch + 2);
+        }
+        si = se;
       }
+      __syncwarp();
     }
     L.H.store(lane);
   }
@@ -826,13 +1089,16 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
       s[3] = st.P;
       s[4] = st.pro_cycles;
       s[5] = clock64() - t0;
-      s[6] = fallback_slices;
+      s[6] = fallback_slices | ((int64_t)p.qs[q].ovf_pages << 20) | ((int64_t)p.qs[q].ovf_pool << 40);
       s[7] = st.wide;
       s[8] = st.pro_cand;
       s[9] = listed;
       s[10] = st.insertions;
       s[11] = __float_as_int(st.hi);
-      for (int j = 12; j < kStats; ++j) s[j] = 0;
+      s[12] = st.pro_t[0];
+      s[13] = st.pro_t[1];
+      s[14] = st.pro_t[2];
+      s[15] = st.pro_t[3];
     }
   }
 }

@@ -25,14 +25,20 @@ struct QState {
   int64_t insertions;
   int64_t pro_cand;     // items the prologue scored in float64
   int64_t pro_cycles;
-  float hi;             // float32 candidate threshold of the filter (x32 < hi)
+  int64_t pro_t[4];     // prologue phase cycles: prefilter, scoring, decisions, blocks
+  int32_t ovf_pages;    // filter slices over kMaxPages (diagnostics)
+  int32_t ovf_pool;     // filter slices that found the pool exhausted
+  double thr;           // filter threshold: candidate iff fast64 < thr
+  uint32_t mtup[2];     // fast-code bytes of the heap item whose fast score is thr
+  int32_t mt_valid;     // (sigma == 0: items with this tuple tie at thr exactly)
+  float lo, hi;         // its certified float32 bounds (x32 < lo: yes, x32 >= hi: no)
   int32_t wide;         // float32 certification off: float64 only
 };
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries)
 constexpr int kMaxPages = 32;    // pages per slice (more -> the replay rescans the slice)
-constexpr int kSliceInts = 1 + kMaxPages;
+constexpr int kSliceInts = 1 + kMaxPages + 3;  // count, page ids, pad to 16 bytes
 constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
 constexpr int64_t kRangeAlign = 32768;  // ranges / padding: whole filter tiles of every warp
@@ -52,7 +58,7 @@ struct PipeParams {
   double* heap_e;             // [Q*k]
   double* heap_f;             // [Q*k]
   int32_t* heap_i;            // [Q*k]
-  uint2* pool;                // [pool_pages * kPG] candidates {id, float32 fast bits}
+  uint4* pool;                // [pool_pages * kPG] candidates {id, f32 fast, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
   int64_t pool_pages;

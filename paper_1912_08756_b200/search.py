@@ -33,7 +33,8 @@ STATS_FIELDS = 16
 STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
                "prologue_cycles", "replay_cycles", "rescanned_slices", "wide",
                "prologue_f64_scored", "filter_candidates", "prologue_insertions",
-               "filter_hi_f32_bits", "reserved12", "reserved13", "reserved14", "reserved15")
+               "filter_hi_f32_bits", "prologue_filter_cycles", "prologue_score_cycles",
+               "prologue_decide_cycles", "prologue_blocks")
 
 
 @dataclass
