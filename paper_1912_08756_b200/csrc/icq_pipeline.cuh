@@ -627,7 +627,6 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         return d;
       }
     };
-    using Mask = typename std::conditional<(V * IPC > 32), unsigned long long, uint32_t>::type;
     int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
     uint4 a[V];
 #pragma unroll
@@ -663,24 +662,40 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           f[v][j] = acc[0];
         }
       }
-      // candidate bits (bit v*IPC + j): x32 < hi; band: not surely (x32 >= lo)
-      Mask cm = 0, bm = 0;
+      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int j = 0; j < IPC; ++j) {
+            const int64_t i = t + (int64_t)(v * 32 + lane) * IPC + j;
+            if (i < start || i >= w_hi) f[v][j] = kInf;
+          }
+      }
+      float lm = f[0][0];
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int j = 0; j < IPC; ++j) lm = fminf(lm, f[v][j]);
+      if (!__any_sync(kFull, lm < hi)) continue;
+      // ---- slow path (most tiles hold a candidate or two) ----
+      using Mask = typename std::conditional<(V * IPC > 32), unsigned long long, uint32_t>::type;
+      // candidate bits (bit v*IPC + j): x32 < hi, except the items whose
+      // fast-code tuple is the threshold item's (fast == thr exactly: never
+      // a candidate; few-codeword books make such ties common).  Everything
+      // kept is a superset of the refined items; the replay decides exactly
+      // with the float64 score of the tuple.
+      Mask cm = 0;
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
         for (int j = 0; j < IPC; ++j) {
-          cm |= (Mask)(f[v][j] < hi ? 1u : 0u) << (v * IPC + j);
-          bm |= (Mask)(f[v][j] >= lo ? 1u : 0u) << (v * IPC + j);
+          bool c = f[v][j] < hi;
+          if constexpr (FP <= 8) {
+            const uint2 tj = chunk_tuple<FP>(x[v], j);
+            c = c && !(mt_valid && tj.x == mtup.x && tj.y == mtup.y);
+          }
+          cm |= (Mask)(c ? 1u : 0u) << (v * IPC + j);
         }
-      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
-#pragma unroll 1
-        for (int idx = 0; idx < V * IPC; ++idx) {
-          const int64_t i = t + (int64_t)((idx / IPC) * 32 + lane) * IPC + (idx % IPC);
-          if (i < start || i >= w_hi) cm &= ~((Mask)1 << idx);
-        }
-      }
-      if (!__any_sync(kFull, cm != 0)) continue;
-      // ---- slow path (most tiles hold a candidate or two): compact loops ----
       auto xsel = [&](int v) {
         uint4 r = x[0];
 #pragma unroll
@@ -688,39 +703,23 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           if (v == vv) r = x[vv];
         return r;
       };
-      // near / exact ties with thr: exact float64 decides (tuple of the
-      // threshold item: fast == thr exactly, never a candidate)
-      bm &= cm;
-      while (bm) {
-        const int idx = (int)__ffsll((unsigned long long)bm) - 1;
-        bm &= bm - 1;
-        const uint4 xv = xsel(idx / IPC);
-        const int j = idx % IPC;
-        bool tie = false;
-        if constexpr (FP <= 8) {
-          const uint2 tj = chunk_tuple<FP>(xv, j);
-          tie = mt_valid && tj.x == mtup.x && tj.y == mtup.y;
-        }
-        if (tie || !(fast_f64(xv, j) < thr)) cm &= ~((Mask)1 << idx);
-      }
-      // per-v counts packed in 16-bit fields -> exclusive prefix over lanes
-      uint32_t cA = 0, cB = 0;
+      // positions in item order (v, lane, j): per v, the (few) lanes holding
+      // candidates take consecutive runs
+      int mybase[V];
+      int g = cnt;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        const uint32_t cc = (uint32_t)__popcll((unsigned long long)((cm >> (v * IPC)) &
-                                                                    (((Mask)1 << IPC) - 1)));
-        if (v < 2) cA |= cc << (16 * v);
-        else cB |= cc << (16 * (v - 2));
+        const int cv = __popcll((unsigned long long)((cm >> (v * IPC)) & (((Mask)1 << IPC) - 1)));
+        uint32_t lanes = __ballot_sync(kFull, cv > 0);
+        mybase[v] = 0;
+        while (lanes) {
+          const int l = __ffs(lanes) - 1;
+          lanes &= lanes - 1;
+          if (lane == l) mybase[v] = g;
+          g += __shfl_sync(kFull, cv, l);
+        }
       }
-      uint32_t iA = cA, iB = cB;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t yA = __shfl_up_sync(kFull, iA, o);
-        const uint32_t yB = __shfl_up_sync(kFull, iB, o);
-        if (lane >= o) { iA += yA; iB += yB; }
-      }
-      const uint32_t tA = __shfl_sync(kFull, iA, 31), tB = __shfl_sync(kFull, iB, 31);
-      const int T = (int)((tA & 0xffffu) + (tA >> 16) + (tB & 0xffffu) + (tB >> 16));
+      const int T = g - cnt;
       if (T == 0) continue;
       const int need = (cnt + T + kPG - 1) / kPG - npages;
       int base_pg = 0;
@@ -740,25 +739,18 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         }
       }
       if (!overflow) {
-        // every lane writes its own entries at its prefix position
-        const uint32_t eA = iA - cA, eB = iB - cB;
-        int curv = -1, g = 0;
+        int curv = -1, gg = 0;
         while (cm) {
           const int idx = (int)__ffsll((unsigned long long)cm) - 1;
           cm &= cm - 1;
           const int v = idx / IPC, j = idx % IPC;
-          if (v != curv) {  // first entry of chunk v: its position
+          if (v != curv) {
             curv = v;
-            const uint32_t tb = (v < 2 ? 0u : ((tA & 0xffffu) + (tA >> 16))) +
-                                (v & 1 ? ((v < 2 ? tA : tB) & 0xffffu) : 0u);
-            g = cnt + (int)tb + (int)(((v < 2 ? eA : eB) >> (16 * (v & 1))) & 0xffffu);
+            gg = mybase[0];
+#pragma unroll
+            for (int vv = 1; vv < V; ++vv)
+              if (vv == v) gg = mybase[vv];
           }
-          float fj = f[0][0];
-#pragma unroll
-          for (int vv = 0; vv < V; ++vv)
-#pragma unroll
-            for (int jj = 0; jj < IPC; ++jj)
-              if (vv * IPC + jj == idx) fj = f[vv][jj];
           const uint4 xv = xsel(v);
           uint2 tail;
           if constexpr (FP <= 8) {
@@ -767,12 +759,11 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
             const unsigned long long db = (unsigned long long)__double_as_longlong(fast_f64(xv, j));
             tail = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
           }
-          const int pi = g / kPG;
+          const int pi = gg / kPG;
           const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
           const int64_t id = t + (int64_t)(v * 32 + lane) * IPC + j;
-          p.pool[(int64_t)pid * kPG + (g % kPG)] =
-              make_uint4((uint32_t)id, __float_as_uint(fj), tail.x, tail.y);
-          ++g;
+          p.pool[(int64_t)pid * kPG + (gg % kPG)] = make_uint4((uint32_t)id, 0u, tail.x, tail.y);
+          ++gg;
         }
         if (need > 0) {
           npages += need;
@@ -1031,7 +1022,7 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
           const int len = min(kCH, total - ch * kCH);
           for (int i = lane; i < len; i += 32) {
             const uint4 ent = src[i];
-            if (__uint_as_float(ent.y) < L.hi)
+            if (entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F) < L.thr64)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(p.codes_full + (int64_t)ent.x * p.KP));
           }
         };
@@ -1058,7 +1049,7 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
               valid[u] = e < len;
               const uint4 ent = valid[u] ? src[e] : make_uint4(0, 0, 0, 0);
               ids[u] = (int32_t)ent.x;
-              fv[u] = __uint_as_float(ent.y);
+              fv[u] = -kInf;  // entries carry no float32 score: float64 from the tuple decides
               tl[u] = make_uint2(ent.z, ent.w);
             }
             replay_window<FP>(L, c, lane, ids, fv, tl, valid, sid, sidx, sfv, lutf);

@@ -58,7 +58,7 @@ struct PipeParams {
   double* heap_e;             // [Q*k]
   double* heap_f;             // [Q*k]
   int32_t* heap_i;            // [Q*k]
-  uint4* pool;                // [pool_pages * kPG] candidates {id, f32 fast, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
+  uint4* pool;                // [pool_pages * kPG] candidates {id, 0, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
   int64_t pool_pages;
