@@ -1001,41 +1001,69 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
           uint4* dst = ring + (ch & 1) * kCH;
           const int v0 = ch * kCH;
           const int len = min(kCH, total - v0);
-          for (int i = lane; i < len; i += 32) {
-            const int v = v0 + i;
-            int lo2 = 0, hi2 = ns;  // slice t with scum[t] <= v < scum[t + 1]
-            while (hi2 - lo2 > 1) {
-              const int mid = (lo2 + hi2) >> 1;
-              if (scum[mid] <= v) lo2 = mid; else hi2 = mid;
+          if (lane < len) {
+            // lane's first entry v0 + lane: slice t with scum[t] <= v < scum[t + 1]
+            // (one search), then 32 entries further per step
+            int ts = 0;
+            {
+              int lo2 = 0, hi2 = ns;
+              const int v = v0 + lane;
+              while (hi2 - lo2 > 1) {
+                const int mid = (lo2 + hi2) >> 1;
+                if (scum[mid] <= v) lo2 = mid; else hi2 = mid;
+              }
+              ts = lo2;
             }
-            const int e = v - scum[lo2];
-            const int32_t* sm = smeta + (si + lo2) * kSliceInts;
-            const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
-                         "l"(src)
-                         : "memory");
+            int e = v0 + lane - scum[ts];
+            int tcnt = scum[ts + 1] - scum[ts];
+            for (int i = lane; i < len; i += 32) {
+              while (e >= tcnt) {
+                e -= tcnt;
+                ++ts;
+                tcnt = scum[ts + 1] - scum[ts];
+              }
+              const int32_t* sm = smeta + (si + ts) * kSliceInts;
+              const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
+                           "l"(src)
+                           : "memory");
+              e += 32;
+            }
           }
           asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        auto prefetch_rows = [&](int ch) {  // rows of the entries refined under the current bound
-          const uint4* src = ring + (ch & 1) * kCH;
+        // chunk arrival: the float64 fast score of every entry (from its
+        // tuple) is written back over the tuple; rows of the entries refined
+        // under the current bound are prefetched
+        auto prep_chunk = [&](int ch) {
+          uint4* src = ring + (ch & 1) * kCH;
           const int len = min(kCH, total - ch * kCH);
           for (int i = lane; i < len; i += 32) {
-            const uint4 ent = src[i];
-            if (entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F) < L.thr64)
+            uint4 ent = src[i];
+            const double f = entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F);
+            const unsigned long long fb = (unsigned long long)__double_as_longlong(f);
+            ent.z = (uint32_t)fb;
+            ent.w = (uint32_t)(fb >> 32);
+            src[i] = ent;
+            if (f < L.thr64)
               asm volatile("prefetch.global.L1 [%0];" ::"l"(p.codes_full + (int64_t)ent.x * p.KP));
           }
+          __syncwarp();
         };
         issue_chunk(0);
-        if (nch > 1) issue_chunk(1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        if (nch > 1) {
+          issue_chunk(1);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk 0 landed
+        } else {
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
         __syncwarp();
-        prefetch_rows(0);
+        prep_chunk(0);
         for (int ch = 0; ch < nch; ++ch) {
           // chunk ch+1 lands first: its rows are prefetched one chunk ahead
           asm volatile("cp.async.wait_group 0;" ::: "memory");
           __syncwarp();
-          if (ch + 1 < nch) prefetch_rows(ch + 1);
+          if (ch + 1 < nch) prep_chunk(ch + 1);
           const uint4* src = ring + (ch & 1) * kCH;
           const int len = min(kCH, total - ch * kCH);
           for (int w0 = 0; w0 < len; w0 += kWU * 32) {
@@ -1052,7 +1080,8 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
               fv[u] = -kInf;  // entries carry no float32 score: float64 from the tuple decides
               tl[u] = make_uint2(ent.z, ent.w);
             }
-            replay_window<FP>(L, c, lane, ids, fv, tl, valid, sid, sidx, sfv, lutf);
+            // tails hold the float64 fast score now (prep_chunk)
+            replay_window<16>(L, c, lane, ids, fv, tl, valid, sid, sidx, sfv, lutf);
           }
           __syncwarp();
           if (ch + 2 < nch) issue_chunk(ch + 2);
