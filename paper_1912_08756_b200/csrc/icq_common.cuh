@@ -262,26 +262,45 @@ struct StaleThr {
   double thr;
   float lo, hi;
 };
-__device__ __forceinline__ StaleThr stale_filter(const Live& L, int F, double sigma, double smin,
-                                                 bool wide, int lane) {
+__device__ __forceinline__ StaleThr stale_core(double M, bool nan, double T, int F, double sigma,
+                                               double smin, bool wide) {
   StaleThr r{__longlong_as_double(0x7ff0000000000000LL), kInf, kInf};
-  if (wide) return r;
-  const double M = L.H.max_fast_all(lane);
-  if (L.H.any_nan_fast(lane)) return r;
+  if (wide || nan) return r;
   double thr;
   if (sigma == 0.0) {
     thr = M;
   } else {
     // (T - Smin) with float64 slack for the different summation orders of
     // fast and exact scores (relative 1e-12 >> K * 2^-53)
-    const double ts = __dsub_ru(L.T64, smin);
-    const double u = fmax(M, __dadd_ru(ts, fabs(L.T64) * 1e-12));
+    const double ts = __dsub_ru(T, smin);
+    const double u = fmax(M, __dadd_ru(ts, fabs(T) * 1e-12));
     thr = __dadd_ru(u, sigma);
   }
   if (!(thr == thr)) return r;
   r.thr = thr;
   certified_bounds(thr, F, r.lo, r.hi);
   return r;
+}
+__device__ __forceinline__ StaleThr stale_filter(const Live& L, int F, double sigma, double smin,
+                                                 bool wide, int lane) {
+  const double M = L.H.max_fast_all(lane);
+  const bool nan = L.H.any_nan_fast(lane);
+  return stale_core(M, nan, L.T64, F, sigma, smin, wide);
+}
+// same, from a heap array in shared memory (any order; entry 0 = maximum), one warp
+__device__ __forceinline__ StaleThr stale_from_heap(const double* he, const double* hf, int k,
+                                                    int F, double sigma, double smin, bool wide,
+                                                    int lane) {
+  double M = -__longlong_as_double(0x7ff0000000000000LL);
+  bool nan = false;
+  for (int i = lane; i < k; i += 32) {
+    M = fmax(M, hf[i]);
+    nan |= !(hf[i] == hf[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+  nan = __any_sync(0xffffffffu, nan);
+  return stale_core(M, nan, he[0], F, sigma, smin, wide);
 }
 
 __device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {

@@ -164,10 +164,11 @@ __host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
 
 constexpr int kWU = 8;  // replay window: kWU x 32 entries
 struct RepLayout {
-  uint32_t lut64, lutf, he, hf, hi, wid, widx, wfv, meta, cum, ring, total;
+  uint32_t lut64, lutf, he, hf, hi, wid, widx, wfv, wfe, meta, cum, chunks, ring, ringe, plist, ctl,
+      total;
 };
 constexpr int kSG = 64;    // slices whose meta the replay stages in shared memory at once
-constexpr int kCH = 1024;  // candidate entries per staged chunk (two chunks in flight)
+constexpr int kCH = 512;   // candidate entries per staged chunk (replay ring slot)
 __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   RepLayout L;
   uint32_t o = 0;
@@ -178,10 +179,15 @@ __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   L.hi = o;    o = al16(o + (uint32_t)k * 4);
   L.wid = o;   o = al16(o + kWU * 32 * 4);
   L.wfv = o;   o = al16(o + kWU * 32 * 8);
+  L.wfe = o;   o = al16(o + kWU * 32 * 8);
   L.widx = o;  o = al16(o + kWU * 32 * 4);
   L.meta = o;  o = al16(o + kSG * kSliceInts * 4);
   L.cum = o;   o = al16(o + (kSG + 1) * 4);
-  L.ring = o;  o = al16(o + 2 * kCH * 16);
+  L.chunks = o; o = al16(o + 512 * 3 * 4);
+  L.ring = o;  o = al16(o + 3 * kCH * 16);
+  L.ringe = o; o = al16(o + 3 * kCH * 8);
+  L.plist = o; o = al16(o + kCH * 4);
+  L.ctl = o;   o = al16(o + 32);
   L.total = o;
   return L;
 }
@@ -289,19 +295,13 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
   __syncthreads();
 
-  Live L;
-  L.refinements = L.insertions = L.candidates = L.certified = 0;
-  L.H.k = k;
-  L.H.reg = k <= 32 * kRegHeapRegs;
-  L.H.he = he;
-  L.H.hf = hf;
-  L.H.hi = hi;
+  // the heap: a binary max-heap by (exact, id) in shared memory (the sorted
+  // seed array is one); thread 0 applies the reference loop serially
+  int64_t refinements = 0, insertions = 0;
   double smin = 0.0;
   if (warp == 0) {
-    L.H.load(lane);
-    live_update(L, F, p.sigma, wide);
     smin = p.sigma == 0.0 ? 0.0 : smin_rd(lut, K, m, p.fast_books, F, lane);
-    const StaleThr t = stale_filter(L, F, p.sigma, smin, wide, lane);
+    const StaleThr t = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
     if (lane == 0) { *pub_lo = t.lo; *pub_hi = t.hi; *pub_thr = t.thr; *flag = k < n ? 1 : 0; }
   }
   __syncthreads();
@@ -402,62 +402,66 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     pro_cand += ncand;
     __syncthreads();
     const long long tc = clock64();
-    // 3d. warp 0 applies search.py:148-154 in order, float64 compares only;
-    //     128-item windows: four 32-item sub-batches tested together, one
-    //     serial round per window up to its first insertion
-    if (warp == 0) {
-      constexpr int U = 4;
-      for (int w0 = 0; w0 < ncand; w0 += 32 * U) {
-        double f[U], e[U];
-        int32_t ids[U];
-        bool valid[U];
+    // 3d. thread 0 applies search.py:148-154 in order (float64 compares):
+    //     refine iff fast < bound + sigma, insert iff exact < T (heapreplace:
+    //     the root is replaced and sifted down; bound = fast of the new root)
+    if (tid == 0) {
+      double T = he[0];
+      double thr = __dadd_rn(hf[0], p.sigma);
+      constexpr int G8 = 8;
+      for (int c0 = 0; c0 < ncand; c0 += G8) {
+        double fg[G8], eg[G8];
+        int32_t ig[G8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = w0 + u * 32 + lane;
-          valid[u] = i < ncand;
-          f[u] = valid[u] ? cf[i] : 0.0;
-          e[u] = valid[u] ? ce[i] : 0.0;
-          ids[u] = valid[u] ? cid[i] : 0;
+        for (int u = 0; u < G8; ++u) {  // all shared-memory loads of the group first
+          const bool ok = c0 + u < ncand;
+          fg[u] = ok ? cf[c0 + u] : 0.0;
+          eg[u] = ok ? ce[c0 + u] : 0.0;
+          ig[u] = ok ? cid[c0 + u] : 0;
         }
-        uint32_t done[U] = {0, 0, 0, 0};
-        for (;;) {
-          uint32_t rm[U], im[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool refined = valid[u] && !((done[u] >> lane) & 1u) && (f[u] < L.thr64);
-            rm[u] = __ballot_sync(kFull, refined);
-            im[u] = __ballot_sync(kFull, refined && (e[u] < L.T64));
-          }
-          int uf = U;  // first sub-batch holding an insertion
+        for (int u = 0; u < G8; ++u) {
+          if (c0 + u >= ncand || !(fg[u] < thr)) continue;
+          const double e = eg[u];
+          const int32_t id = ig[u];
+          ++refinements;
+          record_survivor(c.surv, id);
+          if (!(e < T)) continue;
+          // 4-ary max-heap: replace the root, sift down (children 4i+1..4i+4)
+          int i = 0;
+          for (;;) {
+            const int c1 = 4 * i + 1;
+            if (c1 >= k) break;
+            double be = he[c1];
+            int32_t bi = hi[c1];
+            int cm = c1;
 #pragma unroll
-          for (int u = U - 1; u >= 0; --u)
-            if (im[u]) uf = u;
-          int first = 31;
-          double ne = 0.0, nf = 0.0;
-          int32_t nid = 0;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            uint32_t dec = 0;
-            if (u < uf) dec = kFull;
-            if (u == uf) {
-              first = __ffs(im[u]) - 1;
-              dec = kFull >> (31 - first);
-              ne = __shfl_sync(kFull, e[u], first);
-              nf = __shfl_sync(kFull, f[u], first);
-              nid = __shfl_sync(kFull, ids[u], first);
+            for (int d = 1; d < 4; ++d) {
+              const int cd = c1 + d;
+              if (cd < k) {
+                const double ed = he[cd];
+                const int32_t id2 = hi[cd];
+                if (key_gt(ed, id2, be, bi)) { be = ed; bi = id2; cm = cd; }
+              }
             }
-            L.refinements += __popc(rm[u] & dec);
-            if ((rm[u] & dec) >> lane & 1u) record_survivor(c.surv, ids[u]);
-            done[u] |= dec;
+            if (!key_gt(be, bi, e, id)) break;
+            he[i] = be;
+            hf[i] = hf[cm];
+            hi[i] = bi;
+            i = cm;
           }
-          if (uf == U) break;
-          L.H.replace_max(ne, nid, nf, lane);
-          live_update64(L, p.sigma);
-          ++L.insertions;
+          he[i] = e;
+          hf[i] = fg[u];
+          hi[i] = id;
+          T = he[0];
+          thr = __dadd_rn(hf[0], p.sigma);
+          ++insertions;
         }
       }
-      live_update(L, F, p.sigma, wide);
-      const StaleThr tn = stale_filter(L, F, p.sigma, smin, wide, lane);
+    }
+    __syncwarp();
+    if (warp == 0) {
+      const StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
       const int64_t nb = bend - max(pos, base);
       bool more = bend < n && bend < p.pro_max;
       if (bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
@@ -470,8 +474,22 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     tp[2] += clock64() - tc;
   }
 
-  // 4. hand the state to the filter / replay kernels
-  if (warp == 0) L.H.store(lane);
+  // 4. hand the state to the filter / replay kernels: the heap sorted
+  //    descending by (exact, id) (rank sort through the candidate buffers)
+  __syncthreads();
+  for (int i = tid; i < k; i += kProThreads) {
+    int rank = 0;
+    for (int j = 0; j < k; ++j) rank += key_gt(he[j], hi[j], he[i], hi[i]) ? 1 : 0;
+    ce[rank] = he[i];
+    cf[rank] = hf[i];
+    cid[rank] = hi[i];
+  }
+  __syncthreads();
+  for (int i = tid; i < k; i += kProThreads) {
+    he[i] = ce[i];
+    hf[i] = cf[i];
+    hi[i] = cid[i];
+  }
   __syncthreads();
   if (tid == 0) {
     // sigma == 0: thr = M is the fast score of a heap item; every item with
@@ -497,8 +515,8 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   if (tid == 0) {
     QState st;
     st.P = pos;
-    st.refinements = L.refinements;
-    st.insertions = L.insertions;
+    st.refinements = refinements;
+    st.insertions = insertions;
     st.pro_cand = pro_cand;
     st.pro_cycles = clock64() - t0;
     st.pro_t[0] = tp[0];
@@ -628,19 +646,24 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       }
     };
     int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
+    // 32-bit tile counters and a running chunk pointer (no 64-bit index math per tile)
+    const uint4* cptr = codes + t / IPC + lane;
+    const int ntile = (int)((w_hi - t + TILE - 1) / TILE);
     uint4 a[V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + t / IPC + v * 32 + lane);
-    for (; t < w_hi; t += TILE) {
+    for (int v = 0; v < V; ++v) a[v] = ldg_stream(cptr + v * 32);
+    for (int it = 0; it < ntile; ++it, t += TILE) {
       uint4 x[V];
 #pragma unroll
       for (int v = 0; v < V; ++v) x[v] = a[v];
-      if (t + TILE < w_hi) {
+      cptr += TILE / IPC;
+      if (it + 1 < ntile) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + (t + TILE) / IPC + v * 32 + lane);
+        for (int v = 0; v < V; ++v) a[v] = ldg_stream(cptr + v * 32);
       }
-      if (lane == 0 && t + kPrefetchTiles * TILE < w_hi)
-        prefetch_l2_bulk(codes + (t + kPrefetchTiles * TILE) / IPC, TILE * FP);
+      // L2 bulk prefetch kPrefetchTiles ahead, 4 tiles per request
+      if (lane == 0 && (it & 3) == 0 && it + kPrefetchTiles + 4 <= ntile)
+        prefetch_l2_bulk(cptr - lane + (kPrefetchTiles - 1) * (TILE / IPC), 4 * TILE * FP);
       // one warp tile: 32 lanes x V 16-byte chunks, items (v, lane, j)
       float f[V][IPC];
 #pragma unroll
@@ -688,14 +711,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
 #pragma unroll
       for (int v = 0; v < V; ++v)
 #pragma unroll
-        for (int j = 0; j < IPC; ++j) {
-          bool c = f[v][j] < hi;
-          if constexpr (FP <= 8) {
-            const uint2 tj = chunk_tuple<FP>(x[v], j);
-            c = c && !(mt_valid && tj.x == mtup.x && tj.y == mtup.y);
-          }
-          cm |= (Mask)(c ? 1u : 0u) << (v * IPC + j);
-        }
+        for (int j = 0; j < IPC; ++j)
+          if (f[v][j] < hi) cm |= (Mask)1 << (v * IPC + j);
       auto xsel = [&](int v) {
         uint4 r = x[0];
 #pragma unroll
@@ -703,6 +720,17 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           if (v == vv) r = x[vv];
         return r;
       };
+      if constexpr (FP <= 8) {
+        if (mt_valid) {  // lane-parallel tie check over the few candidate bits
+          Mask mm = cm;
+          while (mm) {
+            const int idx = (int)__ffsll((unsigned long long)mm) - 1;
+            mm &= mm - 1;
+            const uint2 tj = chunk_tuple<FP>(xsel(idx / IPC), idx % IPC);
+            if (tj.x == mtup.x && tj.y == mtup.y) cm &= ~((Mask)1 << idx);
+          }
+        }
+      }
       // positions in item order (v, lane, j): per v, the (few) lanes holding
       // candidates take consecutive runs
       int mybase[V];
@@ -797,8 +825,9 @@ __device__ __forceinline__ double entry_f64(uint2 tail, const double* lutf, int 
 template <int FP>
 __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
                                               const int32_t (&ids)[kWU], const float (&f32)[kWU],
-                                              const uint2 (&tail)[kWU], const bool (&valid)[kWU],
-                                              int32_t* sid, int32_t* sidx, double* sfv,
+                                              const uint2 (&tail)[kWU], const double (&ex)[kWU],
+                                              const bool (&valid)[kWU], int32_t* sid,
+                                              int32_t* sidx, double* sfv, double* sfe,
                                               const double* lutf) {
   int pos0 = 0;  // first undecided window position (u * 32 + lane)
   const uint32_t lt = (1u << lane) - 1u;
@@ -829,6 +858,7 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
         sid[pos] = ids[u];
         sidx[pos] = u * 32 + lane;
         sfv[pos] = d[u];
+        sfe[pos] = ex[u];
       }
     }
     __syncwarp();
@@ -839,8 +869,8 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
       const int32_t id = v ? sid[j] : 0;
       const int32_t wpos = v ? sidx[j] : 0;
       const double f64 = v ? sfv[j] : 0.0;
-      double e64 = 0.0;
-      if (v) e64 = exact64(c.lut, c.m, c.K, c.pw, load_row(c.codes_full, c.KP, id));
+      double e64 = v ? sfe[j] : 0.0;  // precomputed at chunk preparation, NaN = not yet
+      if (v && !(e64 == e64)) e64 = exact64(c.lut, c.m, c.K, c.pw, load_row(c.codes_full, c.KP, id));
       uint32_t done = 0;
       for (;;) {
         const bool refined = v && !((done >> lane) & 1u) && (f64 < L.thr64);
@@ -872,10 +902,21 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
   }
 }
 
+// One CTA per query: warp 0 decides (the in-order reference loop), warps
+// 1..3 prepare.  The candidate slices of a group (kSG slices) are cut into
+// chunks of <= kCH entries (a rescan slice is a chunk of its own); chunk c+2
+// is staged by cp.async, chunk c+1 prepared (float64 fast score from the
+// tuple; exact score of every entry refined under the bound warp 0 last
+// published) and chunk c decided, all at once, one CTA barrier per chunk.
+constexpr int kRW = 4;            // warps per replay CTA
+constexpr int kRP = (kRW - 1) * 32;  // preparing threads
+constexpr int kRSlots = 3;
+constexpr int kMaxChunks = 512;   // chunk descriptors per slice group
+
 template <int FP>
-__global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ PipeParams p) {
+__global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_constant__ PipeParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
   const int K = p.K, m = p.m, F = p.F, k = p.k;
   const int64_t n = p.n;
@@ -887,17 +928,32 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
   int32_t* sid = reinterpret_cast<int32_t*>(dsm + Ly.wid);
   int32_t* sidx = reinterpret_cast<int32_t*>(dsm + Ly.widx);
   double* sfv = reinterpret_cast<double*>(dsm + Ly.wfv);
+  double* sfe = reinterpret_cast<double*>(dsm + Ly.wfe);
   double* lutf = reinterpret_cast<double*>(dsm + Ly.lutf);
   int32_t* smeta = reinterpret_cast<int32_t*>(dsm + Ly.meta);
   int32_t* scum = reinterpret_cast<int32_t*>(dsm + Ly.cum);
+  int32_t* chunk = reinterpret_cast<int32_t*>(dsm + Ly.chunks);  // [kMaxChunks][3]
   uint4* ring = reinterpret_cast<uint4*>(dsm + Ly.ring);
+  double* ring_e = reinterpret_cast<double*>(dsm + Ly.ringe);
+  int32_t* plist = reinterpret_cast<int32_t*>(dsm + Ly.plist);   // prep: live-ish entries
+  volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctl);
+  volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctl + 16);
   const long long t0 = clock64();
   const QState st = p.qs[q];
-  for (int i = lane; i < k; i += 32) {
+  for (int i = tid; i < k; i += kRW * 32) {
     he[i] = p.heap_e[(size_t)q * k + i];
     hf[i] = p.heap_f[(size_t)q * k + i];
     hi[i] = p.heap_i[(size_t)q * k + i];
   }
+  const double* glut = p.lut64 + (size_t)q * K * m;
+  if (st.P < n) {
+    for (int i = tid; i < K * m; i += kRW * 32) lut[i] = glut[i];
+    for (int i = tid; i < F * m; i += kRW * 32) {
+      const int s2 = i / m, j = i - s2 * m;
+      lutf[i] = glut[p.fast_books[s2] * m + j];
+    }
+  }
+  __syncthreads();
   Live L;
   L.refinements = st.refinements;
   L.insertions = st.insertions;
@@ -908,55 +964,161 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
   L.H.hf = hf;
   L.H.hi = hi;
   int64_t fallback_slices = 0, listed = 0;
+  RCtx c;
+  c.lut = lut;
+  c.codes_full = p.codes_full;
+  c.fb = p.fast_books;
+  c.KP = p.KP; c.m = m; c.K = K; c.F = F;
+  c.sigma = p.sigma;
+  c.pw = false;  // n >= 2 whenever the replay runs (P >= k >= 1 and P < n)
+  c.wide = false;
+  c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
   if (st.P < n) {
-    const double* glut = p.lut64 + (size_t)q * K * m;
-    for (int i = lane; i < K * m; i += 32) lut[i] = glut[i];
-    for (int i = lane; i < F * m; i += 32) {
-      const int s = i / m, j = i - s * m;
-      lutf[i] = glut[p.fast_books[s] * m + j];
+    if (warp == 0) {
+      L.H.load(lane);
+      live_update(L, F, p.sigma, false);
+      if (lane == 0) *pub_thr = L.thr64;
     }
-    __syncwarp();
-    L.H.load(lane);
-    live_update(L, F, p.sigma, false);
-    RCtx c;
-    c.lut = lut;
-    c.codes_full = p.codes_full;
-    c.fb = p.fast_books;
-    c.KP = p.KP; c.m = m; c.K = K; c.F = F;
-    c.sigma = p.sigma;
-    c.pw = false;  // n >= 2 here (P >= k >= 1 and P < n)
-    c.wide = false;
-    c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
     const int64_t SW = p.RS / kFW;
     const int NS = p.NR * kFW;  // slices of this query, in database order
     const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
+    const int ptid = tid - 32;  // preparing thread index (warps 1..3)
     for (int g0 = 0; g0 < NS; g0 += kSG) {
       const int ng = min(kSG, NS - g0);
-      // group meta (counts + page ids) -> shared memory, all copies in flight at once
-      {
-        const int chunks = ng * kSliceInts / 4;  // 16-byte pieces
+      {  // group meta (counts + page ids) -> shared memory
+        const int pieces = ng * kSliceInts / 4;
         const uint4* src = reinterpret_cast<const uint4*>(qsl + (int64_t)g0 * kSliceInts);
-        for (int i = lane; i < chunks; i += 32)
+        for (int i = tid; i < pieces; i += kRW * 32)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smeta + 4 * i)),
                        "l"(src + i)
                        : "memory");
         asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncwarp();
       }
-      int si = 0;
-      while (si < ng) {
-        const int cnt0 = smeta[si * kSliceInts];
-        if (cnt0 == 0) { ++si; continue; }
-        if (cnt0 < 0) {
-          // candidates overflowed the slice's pages: rescan its items from the codes
-          int32_t ids2[kWU];
-          float f2[kWU];
-          uint2 t2[kWU];
-          bool valid2[kWU];
-          const int64_t j = g0 + si;
+      __syncthreads();
+      if (tid == 0) {
+        // scum: listed entries before each slice (rescans count 0); chunks:
+        // {first virtual entry, length, -1} or {-, -, rescan slice}
+        int acc = 0, nc = 0, open = -1;
+        for (int t2 = 0; t2 < ng; ++t2) {
+          scum[t2] = acc;
+          const int cnt = smeta[t2 * kSliceInts];
+          if (cnt < 0) {
+            if (nc < kMaxChunks) { chunk[3 * nc] = acc; chunk[3 * nc + 1] = 0; chunk[3 * nc + 2] = t2; ++nc; }
+            open = -1;
+            continue;
+          }
+          int rem = cnt;
+          while (rem > 0) {
+            if (open < 0 || chunk[3 * open + 1] == kCH) {
+              if (nc >= kMaxChunks) break;
+              open = nc++;
+              chunk[3 * open] = acc;
+              chunk[3 * open + 1] = 0;
+              chunk[3 * open + 2] = -1;
+            }
+            const int take = min(rem, kCH - chunk[3 * open + 1]);
+            chunk[3 * open + 1] += take;
+            acc += take;
+            rem -= take;
+          }
+        }
+        scum[ng] = acc;
+        ctl[0] = nc;
+        ctl[1] = nc >= kMaxChunks ? 1 : 0;
+      }
+      __syncthreads();
+      const int nc = ctl[0];
+      if (ctl[1]) {  // more chunks than descriptors: should not happen (kMaxChunks * kCH entries)
+        if (tid == 0) atomicExch(p.error, 4);
+        break;
+      }
+      listed += scum[ng];
+      // ---- preparing warps: stage chunk ch (cp.async) ----
+      auto issue = [&](int ch) {
+        if (ch < nc && chunk[3 * ch + 2] < 0) {
+          uint4* dst = ring + (ch % kRSlots) * kCH;
+          const int v0 = chunk[3 * ch], len = chunk[3 * ch + 1];
+          if (ptid < len) {
+            int lo2 = 0, hi2 = ng;  // slice t: scum[t] <= v < scum[t + 1]
+            const int v = v0 + ptid;
+            while (hi2 - lo2 > 1) {
+              const int mid = (lo2 + hi2) >> 1;
+              if (scum[mid] <= v) lo2 = mid; else hi2 = mid;
+            }
+            int ts = lo2;
+            int e = v - scum[ts];
+            int tcnt = scum[ts + 1] - scum[ts];
+            for (int i = ptid; i < len; i += kRP) {
+              while (e >= tcnt) {
+                e -= tcnt;
+                ++ts;
+                tcnt = scum[ts + 1] - scum[ts];
+              }
+              const int32_t* sm = smeta + ts * kSliceInts;
+              const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
+                           "l"(src)
+                           : "memory");
+              e += kRP;
+            }
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      // ---- preparing warps: float64 fast scores, exact scores of the
+      //      entries refined under the published bound ----
+      auto prep = [&](int ch) {
+        if (ch >= nc || chunk[3 * ch + 2] >= 0) return;
+        uint4* src = ring + (ch % kRSlots) * kCH;
+        double* ex = ring_e + (ch % kRSlots) * kCH;
+        const int len = chunk[3 * ch + 1];
+        const double thr = *pub_thr;
+        for (int i = ptid; i < len; i += kRP) {
+          uint4 ent = src[i];
+          const double f = entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F);
+          const unsigned long long fb = (unsigned long long)__double_as_longlong(f);
+          ent.z = (uint32_t)fb;
+          ent.w = (uint32_t)(fb >> 32);
+          src[i] = ent;
+          ex[i] = __longlong_as_double(0x7ff8000000000000LL);
+          if (f < thr) plist[atomicAdd((int*)&ctl[2], 1)] = i;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+        const int nl = ctl[2];
+        for (int jj = ptid; jj < nl; jj += kRP) {
+          const int idx = plist[jj];
+          ex[idx] = exact64(lut, m, K, false, load_row(p.codes_full, p.KP, (int32_t)src[idx].x));
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+        if (ptid == 0) ctl[2] = 0;
+      };
+      if (warp > 0) {
+        if (ptid == 0) ctl[2] = 0;
+        asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+        issue(0);
+        issue(1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+        prep(0);
+      }
+      __syncthreads();
+      for (int ch = 0; ch < nc; ++ch) {
+        if (warp > 0) {
+          issue(ch + 2);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk ch+1 landed
+          asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+          prep(ch + 1);
+        } else if (chunk[3 * ch + 2] >= 0) {
+          // candidates overflowed this slice's pages: rescan its items from the codes
+          const int64_t j = g0 + chunk[3 * ch + 2];
           const int64_t lo = max(j * SW, st.P), hi_ = min((j + 1) * SW, n);
           if (lo < hi_) ++fallback_slices;
           for (int64_t i0 = lo; i0 < hi_; i0 += kWU * 32) {
+            int32_t ids2[kWU];
+            float f2[kWU];
+            uint2 t2[kWU];
+            double e2[kWU];
+            bool valid2[kWU];
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
               const int64_t i = i0 + u * 32 + lane;
@@ -964,6 +1126,7 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
               ids2[u] = (int32_t)i;
               f2[u] = -kInf;  // no float32 score: the exact float64 one decides
               t2[u] = make_uint2(0u, 0u);
+              e2[u] = __longlong_as_double(0x7ff8000000000000LL);
               if (valid2[u]) {
                 const Row r2 = load_row(p.codes_fast, FP, i);
                 if constexpr (FP <= 8) {
@@ -978,98 +1141,18 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
                 }
               }
             }
-            replay_window<FP>(L, c, lane, ids2, f2, t2, valid2, sid, sidx, sfv, lutf);
+            replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf);
           }
-          ++si;
-          continue;
-        }
-        // a run of listed slices [si, se): one virtual list, staged through
-        // the shared-memory ring in chunks of kCH entries (two in flight)
-        int se = si;
-        while (se < ng && smeta[se * kSliceInts] >= 0) ++se;
-        if (lane == 0) {
-          int acc = 0;
-          for (int t2 = si; t2 < se; ++t2) { scum[t2 - si] = acc; acc += smeta[t2 * kSliceInts]; }
-          scum[se - si] = acc;
-        }
-        __syncwarp();
-        const int ns = se - si;
-        const int total = scum[ns];
-        listed += total;
-        const int nch = (total + kCH - 1) / kCH;
-        auto issue_chunk = [&](int ch) {
-          uint4* dst = ring + (ch & 1) * kCH;
-          const int v0 = ch * kCH;
-          const int len = min(kCH, total - v0);
-          if (lane < len) {
-            // lane's first entry v0 + lane: slice t with scum[t] <= v < scum[t + 1]
-            // (one search), then 32 entries further per step
-            int ts = 0;
-            {
-              int lo2 = 0, hi2 = ns;
-              const int v = v0 + lane;
-              while (hi2 - lo2 > 1) {
-                const int mid = (lo2 + hi2) >> 1;
-                if (scum[mid] <= v) lo2 = mid; else hi2 = mid;
-              }
-              ts = lo2;
-            }
-            int e = v0 + lane - scum[ts];
-            int tcnt = scum[ts + 1] - scum[ts];
-            for (int i = lane; i < len; i += 32) {
-              while (e >= tcnt) {
-                e -= tcnt;
-                ++ts;
-                tcnt = scum[ts + 1] - scum[ts];
-              }
-              const int32_t* sm = smeta + (si + ts) * kSliceInts;
-              const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
-                           "l"(src)
-                           : "memory");
-              e += 32;
-            }
-          }
-          asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        // chunk arrival: the float64 fast score of every entry (from its
-        // tuple) is written back over the tuple; rows of the entries refined
-        // under the current bound are prefetched
-        auto prep_chunk = [&](int ch) {
-          uint4* src = ring + (ch & 1) * kCH;
-          const int len = min(kCH, total - ch * kCH);
-          for (int i = lane; i < len; i += 32) {
-            uint4 ent = src[i];
-            const double f = entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F);
-            const unsigned long long fb = (unsigned long long)__double_as_longlong(f);
-            ent.z = (uint32_t)fb;
-            ent.w = (uint32_t)(fb >> 32);
-            src[i] = ent;
-            if (f < L.thr64)
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(p.codes_full + (int64_t)ent.x * p.KP));
-          }
-          __syncwarp();
-        };
-        issue_chunk(0);
-        if (nch > 1) {
-          issue_chunk(1);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk 0 landed
+          if (lane == 0) *pub_thr = L.thr64;
         } else {
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-        }
-        __syncwarp();
-        prep_chunk(0);
-        for (int ch = 0; ch < nch; ++ch) {
-          // chunk ch+1 lands first: its rows are prefetched one chunk ahead
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-          __syncwarp();
-          if (ch + 1 < nch) prep_chunk(ch + 1);
-          const uint4* src = ring + (ch & 1) * kCH;
-          const int len = min(kCH, total - ch * kCH);
+          const uint4* src = ring + (ch % kRSlots) * kCH;
+          const double* exs = ring_e + (ch % kRSlots) * kCH;
+          const int len = chunk[3 * ch + 1];
           for (int w0 = 0; w0 < len; w0 += kWU * 32) {
             int32_t ids[kWU];
             float fv[kWU];
             uint2 tl[kWU];
+            double exv[kWU];
             bool valid[kWU];
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
@@ -1077,29 +1160,29 @@ __global__ void __launch_bounds__(32) icq_replay_kernel(const __grid_constant__ 
               valid[u] = e < len;
               const uint4 ent = valid[u] ? src[e] : make_uint4(0, 0, 0, 0);
               ids[u] = (int32_t)ent.x;
-              fv[u] = -kInf;  // entries carry no float32 score: float64 from the tuple decides
+              fv[u] = -kInf;  // float64 fast score in .z/.w (prep) decides
               tl[u] = make_uint2(ent.z, ent.w);
+              exv[u] = valid[u] ? exs[e] : 0.0;
             }
-            // tails hold the float64 fast score now (prep_chunk)
-            replay_window<16>(L, c, lane, ids, fv, tl, valid, sid, sidx, sfv, lutf);
+            replay_window<16>(L, c, lane, ids, fv, tl, exv, valid, sid, sidx, sfv, sfe, lutf);
           }
-          __syncwarp();
-          if (ch + 2 < nch) issue_chunk(ch + 2);
+          if (lane == 0) *pub_thr = L.thr64;
         }
-        si = se;
+        __syncthreads();
       }
-      __syncwarp();
+      if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
     }
-    L.H.store(lane);
+    if (warp == 0) L.H.store(lane);
   }
-  __syncwarp();
+  __syncthreads();
   // output: heap ascending by (score, id) (search.py:156-165)
-  for (int i = lane; i < k; i += 32) {
+  for (int i = tid; i < k; i += kRW * 32) {
     const int src = k - 1 - i;
     p.ids[(size_t)q * k + i] = hi[src];
     p.scores[(size_t)q * k + i] = he[src];
   }
-  if (lane == 0) {
+  if (tid == 0) {
     if (p.refinements) p.refinements[q] = p.exact_mode ? n : L.refinements;
     if (p.stats) {
       int64_t* s = p.stats + (size_t)q * kStats;
@@ -1149,7 +1232,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s,
   icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[2], s);
-  icq_replay_kernel<FP><<<p.Q, 32, rl.total, s>>>(p);
+  icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[3], s);
   return cudaSuccess;
