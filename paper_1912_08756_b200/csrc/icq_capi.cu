@@ -24,7 +24,8 @@ static thread_local std::string g_err;
 // CUDA events recorded on the launch stream around each pipeline kernel.
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
-static std::vector<cudaEvent_t> g_prof_events;  // groups of 4 per launch
+static std::vector<cudaEvent_t> g_prof_events;  // groups of kProfEvents per batch
+static constexpr int kProfEvents = 2 + 2 * icq::kRounds;
 
 static icq_status fail(icq_status code, const char* fmt, ...) {
   char buf[512];
@@ -206,16 +207,16 @@ icq_status icq_profile_enable(int32_t on) {
 
 icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   std::lock_guard<std::mutex> g(g_prof_mu);
-  double acc[3] = {0, 0, 0};
-  const int groups = (int)(g_prof_events.size() / 4);
+  double acc[3] = {0, 0, 0};  // prologue, filter (all rounds), replay (all rounds)
+  const int groups = (int)(g_prof_events.size() / kProfEvents);
   for (int i = 0; i < groups; ++i) {
-    cudaEvent_t* e = &g_prof_events[4 * i];
-    if (cudaEventSynchronize(e[3]) != cudaSuccess)
+    cudaEvent_t* e = &g_prof_events[kProfEvents * i];
+    if (cudaEventSynchronize(e[kProfEvents - 1]) != cudaSuccess)
       return fail(ICQ_ERR_CUDA, "profile: event synchronize failed");
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j + 1 < kProfEvents; ++j) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e[j], e[j + 1]);
-      acc[j] += ms;
+      acc[j == 0 ? 0 : (j % 2 == 1 ? 1 : 2)] += ms;
     }
   }
   for (cudaEvent_t e : g_prof_events) cudaEventDestroy(e);
@@ -366,6 +367,13 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.NR = (int32_t)((h->n + rs - 1) / rs);
   }
   p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 256);
+  p.debug = (int32_t)env_i("ICQ_DEBUG", 0);  // experiments only; results stay exact
+  p.j0 = (int32_t)env_i("ICQ_J0", -1);        // tests: force the first-round insertion budget
+  {
+    // insertion-budgeted filter rounds (experimental; 1 = one round with M)
+    int64_t r = env_i("ICQ_ROUNDS", 1);
+    p.max_rounds = (int32_t)(r < 1 ? 1 : (r > kRounds ? kRounds : r));
+  }
   p.pro_min = env_i("ICQ_PRO_MIN", 8192);
   {
     int64_t pm = h->n / 16;
@@ -393,7 +401,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   const size_t b_qs = al(sizeof(QState) * Qb);
   const size_t b_he = al((size_t)Qb * k * 8), b_hi = al((size_t)Qb * k * 4);
   const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint4));
-  const size_t b_top = 256;
+  const size_t b_top = 256;  // pool_top + active[kRounds]
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
   const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl;
   char* sc = nullptr;
@@ -405,7 +413,9 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.heap_f = reinterpret_cast<double*>(o); o += b_he;
     p.heap_i = reinterpret_cast<int32_t*>(o); o += b_hi;
     p.pool = reinterpret_cast<uint4*>(o); o += b_pool;
-    p.pool_top = reinterpret_cast<int32_t*>(o); o += b_top;
+    p.pool_top = reinterpret_cast<int32_t*>(o);
+    p.active = p.pool_top + 1;
+    o += b_top;
     p.slices = reinterpret_cast<int32_t*>(o);
   }
   icq_status st = ICQ_OK;
@@ -419,14 +429,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     b.refinements = refine ? refine + q0 : nullptr;
     b.survivors = (!exact && survivors) ? survivors + (size_t)q0 * p.words : nullptr;
     b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
-    cudaError_t e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
+    cudaError_t e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t) * (1 + kRounds), s);
     int unsupported = 0;
     cudaEvent_t* ev = nullptr;
-    cudaEvent_t evs[4];
+    cudaEvent_t evs[kProfEvents];
     {
       std::lock_guard<std::mutex> g(g_prof_mu);
       if (g_prof_on) {
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kProfEvents; ++j) {
           cudaEventCreate(&evs[j]);
           g_prof_events.push_back(evs[j]);
         }

@@ -41,6 +41,7 @@
 namespace icq {
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kSelectJ = 40;  // prologue: budgeted prefilter only for budgets below this
 
 // --------------------------------------------------------------------------
 // decision context shared by the prologue and replay warps
@@ -53,6 +54,8 @@ struct RCtx {
   double sigma;
   bool pw, wide;
   uint32_t* surv;
+  int64_t ins_limit;     // the filter threshold holds up to this many insertions
+  int64_t* stop_pos;     // shared: first undecided item when the budget ran out
 };
 
 struct Decided {
@@ -187,7 +190,7 @@ __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   L.ring = o;  o = al16(o + 3 * kCH * 16);
   L.ringe = o; o = al16(o + 3 * kCH * 8);
   L.plist = o; o = al16(o + kCH * 4);
-  L.ctl = o;   o = al16(o + 32);
+  L.ctl = o;   o = al16(o + 64);
   L.total = o;
   return L;
 }
@@ -232,6 +235,10 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   volatile float* pub_hi = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 68);
   volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctrl + 72);
   volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctrl + 80);
+  int* band_total = reinterpret_cast<int*>(dsm + Ly.ctrl + 96);  // near-ties seen by the prefilter
+  volatile int* ins_recent = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 100);  // last 4 blocks
+  volatile int* pub_J = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 104);  // prefilter budget
+  volatile long long* cut = reinterpret_cast<volatile long long*>(dsm + Ly.ctrl + 112);  // pass end
   const long long t0 = clock64();
 
   // 1. float64 LUT -> smem, float32 copy of the fast books (prefilter)
@@ -302,7 +309,13 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   if (warp == 0) {
     smin = p.sigma == 0.0 ? 0.0 : smin_rd(lut, K, m, p.fast_books, F, lane);
     const StaleThr t = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
-    if (lane == 0) { *pub_lo = t.lo; *pub_hi = t.hi; *pub_thr = t.thr; *flag = k < n ? 1 : 0; }
+    if (lane == 0) {
+      *pub_lo = t.lo; *pub_hi = t.hi; *pub_thr = t.thr; *flag = k < n ? 1 : 0;
+      *band_total = 0;
+      *ins_recent = 0;
+      *pub_J = kInfBudget;
+      *cut = -1;
+    }
   }
   __syncthreads();
 
@@ -311,6 +324,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   int64_t pro_cand = 0;
   long long tp[3] = {0, 0, 0};
   int64_t nblocks = 0;
+  int ins_hist[4] = {0, 0, 0, 0};  // thread 0: insertions of the last four blocks
   while (*flag) {
     const long long ta = clock64();
     ++nblocks;
@@ -335,6 +349,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       }
     }
     uint32_t mask = 0;
+    int nband = 0;  // items float32 could not decide (near / exact ties with the threshold)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float x = 0.f;
@@ -347,6 +362,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       const int64_t i = i0 + j;
       bool cand = wide || x < hl;
       if (!cand && x < h) {  // float32 cannot decide: exact float64 fast score
+        nband += (i0 + j >= pos) & (i0 + j < bend);
         double d = 0.0;
 #pragma unroll
         for (int s = 0; s < FP; ++s) {
@@ -359,6 +375,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       mask |= ((i >= pos) & (i < bend) & cand) ? (1u << j) : 0u;
     }
     // 3b. ordered compaction (thread order = item order)
+    if (nband) atomicAdd(band_total, nband);
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll
@@ -406,6 +423,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     //     refine iff fast < bound + sigma, insert iff exact < T (heapreplace:
     //     the root is replaced and sifted down; bound = fast of the new root)
     if (tid == 0) {
+      const int64_t ins_before = insertions;
+      const int64_t ins_limit = *pub_J >= kInfBudget ? INT64_MAX : insertions + *pub_J;
+      *cut = -1;
       double T = he[0];
       double thr = __dadd_rn(hf[0], p.sigma);
       constexpr int G8 = 8;
@@ -456,19 +476,68 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
           T = he[0];
           thr = __dadd_rn(hf[0], p.sigma);
           ++insertions;
+          if (insertions > ins_limit) {  // the prefilter threshold is spent: re-filter the rest
+            *cut = (long long)id + 1;
+            break;
+          }
         }
+        if (*cut >= 0) break;
       }
+      ins_hist[nblocks & 3] = (int)(insertions - ins_before);
+      *ins_recent = ins_hist[0] + ins_hist[1] + ins_hist[2] + ins_hist[3];
     }
     __syncwarp();
     if (warp == 0) {
-      const StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
-      const int64_t nb = bend - max(pos, base);
-      bool more = bend < n && bend < p.pro_max;
-      if (bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
-      if (lane == 0) { *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *flag = more ? 1 : 0; }
+      StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
+      // insertions have become rare: prefilter (and later filter) with the
+      // budgeted A_J (max fast over the J+1 largest-exact entries), far
+      // tighter than M when a high-fast item sits deep in the heap
+      const int Jc = (*ins_recent) * 2;  // 0 once insertions have stopped: A_0 = the live bound
+      int Jpub = kInfBudget;
+      if (p.max_rounds > 1 && p.sigma == 0.0 && !wide && nblocks >= 4 && Jc < kSelectJ &&
+          Jc < k - 1) {
+        double A = -__longlong_as_double(0x7ff0000000000000LL);
+        double pe = __longlong_as_double(0x7ff0000000000000LL);
+        int32_t pi = 0x7fffffff;
+        int Jt = 0;
+        for (int r = 0; r <= Jc; ++r) {  // r-th largest (exact, id): warp argmax below the last
+          double be = -__longlong_as_double(0x7ff0000000000000LL), bf = 0.0;
+          int32_t bi = -1;
+          for (int i = lane; i < k; i += 32) {
+            const double e2 = he[i];
+            const int32_t i2 = hi[i];
+            if (key_gt(pe, pi, e2, i2) && (bi < 0 || key_gt(e2, i2, be, bi))) { be = e2; bi = i2; bf = hf[i]; }
+          }
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const double oe = __shfl_xor_sync(kFull, be, o);
+            const int32_t oi = __shfl_xor_sync(kFull, bi, o);
+            const double of = __shfl_xor_sync(kFull, bf, o);
+            if (oi >= 0 && (bi < 0 || key_gt(oe, oi, be, bi))) { be = oe; bi = oi; bf = of; }
+          }
+          pe = be;
+          pi = bi;
+          A = fmax(A, bf);
+          Jt = r;
+        }
+        if (A < tn.thr) {
+          tn.thr = A;
+          certified_bounds(A, F, tn.lo, tn.hi);
+          Jpub = Jt;
+        }
+      }
+      const bool stopped = *cut >= 0;
+      const int64_t pend = stopped ? (int64_t)*cut : bend;
+      const int64_t nb = pend - max(pos, base);
+      bool more = pend < n && pend < p.pro_max;
+      if (!stopped && bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
+      if (lane == 0) {
+        *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *pub_J = Jpub;
+        *flag = more ? 1 : 0;
+      }
     }
-    pos = bend;
     __syncthreads();
+    pos = *cut >= 0 ? (int64_t)*cut : bend;
     tp[0] += tb - ta;
     tp[1] += tc - tb;
     tp[2] += clock64() - tc;
@@ -492,27 +561,41 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
   __syncthreads();
   if (tid == 0) {
-    // sigma == 0: thr = M is the fast score of a heap item; every item with
-    // its fast-code tuple ties at thr exactly (never a candidate)
+    // The filter threshold for the rest of the database.  sigma == 0: A_J =
+    // max fast over the J+1 largest-exact heap entries bounds the live bound
+    // for the next J insertions (they evict entries in exact order; an
+    // inserted item has fast < bound), so with J sized from the recent
+    // insertion rate it is far tighter than M = A_{k-1} when a high-fast item
+    // sits deep in the heap.  The replay stops when the budget runs out and
+    // the next round re-filters the rest.  sigma > 0: U + sigma, unbudgeted.
+    const int rate = *ins_recent;
+    int J = p.j0 >= 0 ? p.j0 : rate * 2;
+    if (p.j0 < 0 && *pub_J >= kInfBudget) J = kInfBudget;  // M was the tighter threshold
     int best = -1;
-    for (int i = 0; i < k; ++i)
-      if (best < 0 || hf[i] > hf[best]) best = i;
+    double thr = *pub_thr;
+    float flo = *pub_lo, fhi = *pub_hi;
+    if (p.max_rounds <= 1) J = kInfBudget;  // single round: M, valid for every later item
+    if (!wide && p.sigma == 0.0) {
+      if (J >= k - 1) J = kInfBudget;
+      const int top = J == kInfBudget ? k : J + 1;
+      best = 0;
+      for (int i = 1; i < top; ++i)
+        if (hf[i] > hf[best]) best = i;
+      thr = hf[best];
+      certified_bounds(thr, F, flo, fhi);
+    } else {
+      J = kInfBudget;
+    }
+    // tie rejection costs the filter a tuple compare per candidate: enabled
+    // only where the prologue saw near-ties in bulk (few-codeword books);
+    // items with the threshold item's fast-code tuple tie at thr exactly
+    const bool ties = (int64_t)(*band_total) * 2048 > pos && !(p.debug & 1);
+    const bool ok = ties && FP <= 8 && best >= 0;
     uint2 tup = make_uint2(0u, 0u);
-    const bool ok = p.sigma == 0.0 && !wide && FP <= 8 && best >= 0 && hf[best] == *pub_thr;
     if (ok) {
       const Row r = load_row(p.codes_fast, FP, hi[best]);
       tup = make_uint2(r.w[0], r.w[1]);
     }
-    wsum[0] = (int32_t)tup.x;
-    wsum[1] = (int32_t)tup.y;
-    wsum[2] = ok ? 1 : 0;
-  }
-  for (int i = tid; i < k; i += kProThreads) {
-    p.heap_e[(size_t)q * k + i] = he[i];
-    p.heap_f[(size_t)q * k + i] = hf[i];
-    p.heap_i[(size_t)q * k + i] = hi[i];
-  }
-  if (tid == 0) {
     QState st;
     st.P = pos;
     st.refinements = refinements;
@@ -523,16 +606,25 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     st.pro_t[1] = tp[1];
     st.pro_t[2] = tp[2];
     st.pro_t[3] = nblocks;
-    st.hi = *pub_hi;
-    st.lo = *pub_lo;
-    st.thr = *pub_thr;
-    st.mtup[0] = (uint32_t)wsum[0];
-    st.mtup[1] = (uint32_t)wsum[1];
-    st.mt_valid = wsum[2];
+    st.hi = fhi;
+    st.lo = flo;
+    st.thr = thr;
+    st.mtup[0] = tup.x;
+    st.mtup[1] = tup.y;
+    st.mt_valid = ok ? 1 : 0;
     st.wide = wide ? 1 : 0;
     st.ovf_pages = 0;
     st.ovf_pool = 0;
+    st.J = J;
+    st.ins0 = insertions;
+    st.done = 0;
+    st.rounds = 0;
     p.qs[q] = st;
+  }
+  for (int i = tid; i < k; i += kProThreads) {
+    p.heap_e[(size_t)q * k + i] = he[i];
+    p.heap_f[(size_t)q * k + i] = hf[i];
+    p.heap_i[(size_t)q * k + i] = hi[i];
   }
 }
 
@@ -574,21 +666,24 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
 
+  if (p.round > 0 && *(volatile int32_t*)&p.active[p.round - 1] == 0) return;  // all finished
   const int K = p.K, m = p.m, F = p.F;
   const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
   const int64_t U = (int64_t)p.Q * p.NR;
   int64_t u0, u1, ustep;
-  if (p.range_major) {  // all CTAs sweep the ranges together: codes reused in L2
+  const bool rmaj = p.range_major || p.round > 0;
+  if (rmaj) {  // all CTAs sweep the ranges together: codes reused in L2, and in later
+               // rounds the few unfinished queries spread over all SMs
     u0 = blockIdx.x; u1 = U; ustep = gridDim.x;
-  } else {              // contiguous unit blocks: one query's LUT serves many units
+  } else {     // contiguous unit blocks: one query's LUT serves many units
     u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1;
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
   int cur_q = -1;
   for (int64_t u = u0; u < u1; u += ustep) {
-    const int q = p.range_major ? (int)(u % p.Q) : (int)(u / p.NR);
-    const int r = p.range_major ? (int)(u / p.Q) : (int)(u % p.NR);
+    const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
+    const int r = rmaj ? (int)(u / p.Q) : (int)(u % p.NR);
     const int64_t P = p.qs[q].P;
     const float hi = p.qs[q].hi, lo = p.qs[q].lo;
     const double thr = p.qs[q].thr;
@@ -597,7 +692,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const int wide = p.qs[q].wide;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
-    if (P >= r_hi) {  // decided by the prologue
+    if (P >= r_hi || p.qs[q].done) {  // decided by the prologue / an earlier round
       if (lane == 0) slice[0] = 0;
       continue;
     }
@@ -685,15 +780,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           f[v][j] = acc[0];
         }
       }
-      if (t < start || t + TILE > w_hi) {  // edge tiles: items outside [start, w_hi)
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-#pragma unroll
-          for (int j = 0; j < IPC; ++j) {
-            const int64_t i = t + (int64_t)(v * 32 + lane) * IPC + j;
-            if (i < start || i >= w_hi) f[v][j] = kInf;
-          }
-      }
+      // (edge tiles: items outside [start, w_hi) are dropped from the
+      // candidate bits below; the cheap minimum test may fire spuriously there)
       float lm = f[0][0];
 #pragma unroll
       for (int v = 0; v < V; ++v)
@@ -713,6 +801,17 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
 #pragma unroll
         for (int j = 0; j < IPC; ++j)
           if (f[v][j] < hi) cm |= (Mask)1 << (v * IPC + j);
+      if (t < start || t + TILE > w_hi) {  // edge tile: keep items in [start, w_hi)
+        const int lo_t = (int)(start - t), hi_t = (int)min((int64_t)TILE, w_hi - t);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int c0 = (v * 32 + lane) * IPC;  // first item of chunk v, relative to t
+          const int a0 = min(max(lo_t - c0, 0), IPC), a1 = min(max(hi_t - c0, 0), IPC);
+          const Mask keep = (a1 > a0) ? (((((Mask)1 << (a1 - a0)) - 1) << a0) << (v * IPC)) : (Mask)0;
+          const Mask band = (((Mask)1 << IPC) - 1) << (v * IPC);
+          cm &= ~band | keep;
+        }
+      }
       auto xsel = [&](int v) {
         uint4 r = x[0];
 #pragma unroll
@@ -823,7 +922,7 @@ __device__ __forceinline__ double entry_f64(uint2 tail, const double* lutf, int 
 // inserted (search.py:152-154).  An insertion moves the bound (up or down):
 // when it rises, the items after the insertion are compacted again.
 template <int FP>
-__device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
+__device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
                                               const int32_t (&ids)[kWU], const float (&f32)[kWU],
                                               const uint2 (&tail)[kWU], const double (&ex)[kWU],
                                               const bool (&valid)[kWU], int32_t* sid,
@@ -850,7 +949,7 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
       base[u] = tot;
       tot += __popc(lm[u]);
     }
-    if (tot == 0) return;
+    if (tot == 0) return false;
 #pragma unroll
     for (int u = 0; u < kWU; ++u) {
       if ((lm[u] >> lane) & 1u) {
@@ -890,6 +989,11 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
         L.H.replace_max(ne, nid, nf, lane);
         live_update(L, c.F, c.sigma, false);
         ++L.insertions;
+        if (L.insertions > c.ins_limit) {  // budget spent: later lists may be incomplete
+          if (lane == 0) *c.stop_pos = (int64_t)nid + 1;
+          __syncwarp();
+          return true;
+        }
         if (L.thr64 > thr) {  // bound rose: re-compact everything after the insertion
           pos0 = __shfl_sync(kFull, wpos, first) + 1;
           restart = true;
@@ -898,7 +1002,7 @@ __device__ __forceinline__ void replay_window(Live& L, const RCtx& c, int lane,
       }
     }
     __syncwarp();
-    if (!restart) return;
+    if (!restart) return false;
   }
 }
 
@@ -940,6 +1044,8 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
   volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctl + 16);
   const long long t0 = clock64();
   const QState st = p.qs[q];
+  if (st.done) return;  // finished in an earlier round
+  int64_t* stop_pos = reinterpret_cast<int64_t*>(dsm + Ly.ctl + 24);
   for (int i = tid; i < k; i += kRW * 32) {
     he[i] = p.heap_e[(size_t)q * k + i];
     hf[i] = p.heap_f[(size_t)q * k + i];
@@ -973,6 +1079,9 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
   c.pw = false;  // n >= 2 whenever the replay runs (P >= k >= 1 and P < n)
   c.wide = false;
   c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
+  c.ins_limit = st.J >= kInfBudget ? INT64_MAX : st.ins0 + st.J;
+  c.stop_pos = stop_pos;
+  if (tid == 0) { ctl[3] = 0; *stop_pos = n; }
   if (st.P < n) {
     if (warp == 0) {
       L.H.load(lane);
@@ -1141,7 +1250,10 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
                 }
               }
             }
-            replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf);
+            if (replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf)) {
+              if (lane == 0) ctl[3] = 1;
+              break;
+            }
           }
           if (lane == 0) *pub_thr = L.thr64;
         } else {
@@ -1164,18 +1276,65 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
               tl[u] = make_uint2(ent.z, ent.w);
               exv[u] = valid[u] ? exs[e] : 0.0;
             }
-            replay_window<16>(L, c, lane, ids, fv, tl, exv, valid, sid, sidx, sfv, sfe, lutf);
+            if (replay_window<16>(L, c, lane, ids, fv, tl, exv, valid, sid, sidx, sfv, sfe, lutf)) {
+              if (lane == 0) ctl[3] = 1;
+              break;
+            }
           }
           if (lane == 0) *pub_thr = L.thr64;
         }
         __syncthreads();
+        if (ctl[3]) break;  // insertion budget spent: the next round resumes at *stop_pos
       }
       if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
+      if (ctl[3]) break;
     }
     if (warp == 0) L.H.store(lane);
   }
   __syncthreads();
+  if (ctl[3]) {
+    // budget spent: hand the state to the next round (heap sorted descending,
+    // resume position, a fresh threshold with 4x the budget, unbudgeted M in
+    // the last round)
+    for (int i = tid; i < k; i += kRW * 32) {
+      p.heap_e[(size_t)q * k + i] = he[i];
+      p.heap_f[(size_t)q * k + i] = hf[i];
+      p.heap_i[(size_t)q * k + i] = hi[i];
+    }
+    if (tid == 0) {
+      QState ns = st;
+      ns.P = *stop_pos;
+      ns.refinements = L.refinements;
+      ns.insertions = L.insertions;
+      ns.ins0 = L.insertions;
+      int J = (p.round + 2 >= p.max_rounds || st.J >= kInfBudget / 4) ? kInfBudget
+                                                                       : max(4, 2 * (st.J + 1));
+      if (J >= k - 1) J = kInfBudget;
+      const int top = J == kInfBudget ? k : J + 1;
+      int best = 0;
+      for (int i = 1; i < top; ++i)
+        if (hf[i] > hf[best]) best = i;
+      ns.J = J;
+      ns.thr = hf[best];
+      certified_bounds(ns.thr, F, ns.lo, ns.hi);
+      if (st.mt_valid) {
+        const Row r = load_row(p.codes_fast, FP, hi[best]);
+        ns.mtup[0] = r.w[0];
+        ns.mtup[1] = r.w[1];
+      }
+      ns.rounds = st.rounds + 1;
+      ns.ovf_pages = 0;
+      ns.ovf_pool = 0;
+      p.qs[q] = ns;
+      atomicAdd(&p.active[p.round], 1);
+    }
+    return;
+  }
+  if (tid == 0) {
+    p.qs[q].done = 1;
+    p.qs[q].P = n;  // later filter rounds skip this query
+  }
   // output: heap ascending by (score, id) (search.py:156-165)
   for (int i = tid; i < k; i += kRW * 32) {
     const int src = k - 1 - i;
@@ -1188,7 +1347,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       int64_t* s = p.stats + (size_t)q * kStats;
       s[0] = L.insertions;
       s[1] = L.candidates;
-      s[2] = L.certified;
+      s[2] = st.rounds + 1;  // filter/replay rounds this query used
       s[3] = st.P;
       s[4] = st.pro_cycles;
       s[5] = clock64() - t0;
@@ -1210,8 +1369,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
 // host launch
 // --------------------------------------------------------------------------
 template <int FP>
-cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s,
-                             cudaEvent_t* ev) {
+cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cudaEvent_t* ev) {
   using G = FGeo<FP>;
   const ProLayout pl = pro_layout(p.K, p.m, p.F, p.k);
   const RepLayout rl = rep_layout(p.K, p.m, p.F, p.k);
@@ -1229,12 +1387,23 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s,
   icq_prologue_kernel<FP><<<p.Q, kProThreads, pl.total, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (ev) cudaEventRecord(ev[2], s);
-  icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(p);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (ev) cudaEventRecord(ev[3], s);
+  // filter / replay rounds: a query whose insertion budget ran out resumes
+  // in the next round; finished queries cost the later launches nothing
+  for (int r = 0; r < p.max_rounds; ++r) {
+    PipeParams pr = p;
+    pr.round = r;
+    if (r > 0 && (e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
+    icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[2 + 2 * r], s);
+    icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(pr);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[3 + 2 * r], s);
+  }
+  for (int r = p.max_rounds; ev && r < kRounds; ++r) {  // unused rounds: empty intervals
+    cudaEventRecord(ev[2 + 2 * r], s);
+    cudaEventRecord(ev[3 + 2 * r], s);
+  }
   return cudaSuccess;
 }
 

@@ -33,12 +33,18 @@ struct QState {
   int32_t mt_valid;     // (sigma == 0: items with this tuple tie at thr exactly)
   float lo, hi;         // its certified float32 bounds (x32 < lo: yes, x32 >= hi: no)
   int32_t wide;         // float32 certification off: float64 only
+  int32_t J;            // insertion budget of thr (kInfBudget: always valid)
+  int64_t ins0;         // insertions when thr was set
+  int32_t done;         // all items decided, outputs written
+  int32_t rounds;       // filter/replay rounds used
 };
+constexpr int32_t kInfBudget = 1 << 30;
+constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries)
-constexpr int kMaxPages = 32;    // pages per slice (more -> the replay rescans the slice)
-constexpr int kSliceInts = 1 + kMaxPages + 3;  // count, page ids, pad to 16 bytes
+constexpr int kMaxPages = 64;    // pages per slice (more -> the replay rescans the slice)
+constexpr int kSliceInts = 4 + kMaxPages;  // count, 3 pad, page ids (16-byte rows)
 constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
 constexpr int64_t kRangeAlign = 32768;  // ranges / padding: whole filter tiles of every warp
@@ -61,6 +67,7 @@ struct PipeParams {
   uint4* pool;                // [pool_pages * kPG] candidates {id, 0, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
+  int32_t* active;            // [kRounds] queries handed to round r+1 by the replay of round r
   int64_t pool_pages;
   int64_t n;
   int64_t words;              // survivors bitmap words per query
@@ -71,6 +78,10 @@ struct PipeParams {
   int32_t range_major;        // filter unit order (L2 reuse of codes larger than L2)
   int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
   int32_t pro_div;            // prologue stops once a block's candidates <= items / pro_div
+  int32_t debug;              // experiments only (ICQ_DEBUG): bit 0 = no tuple-tie rejection
+  int32_t round;              // current filter/replay round (0-based)
+  int32_t j0;                 // first-round insertion budget (-1: from the insertion rate)
+  int32_t max_rounds;         // filter/replay rounds (1: no insertion budgets, threshold M)
   int64_t pro_min, pro_max;   // prologue length bounds (items)
   uint8_t fast_books[kMaxK];
 };
@@ -79,7 +90,8 @@ bool make_lut_prog(int d, LutProg* out);
 cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, int m, int d,
                        int Q, const LutProg* prog_dev, cudaStream_t s);
 // prologue -> filter -> replay for one batch (icq_pipeline.cu)
-// ev: optional 4 events recorded before the prologue, filter, replay and after it
+// ev: optional 2 + 2 * kRounds events: before/after the prologue, then after the
+// filter and after the replay of every round
 cudaError_t launch_pipeline(const PipeParams& p, int FP, int filter_ctas, cudaStream_t s,
                             int* unsupported, cudaEvent_t* ev = nullptr);
 

@@ -83,11 +83,17 @@ CONFIGS = [
 #   overflow  - as filter, with a 2-page candidate pool: slices overflow and
 #               the replay rescans them from the codes
 #   subbatch  - as filter, queries in sub-batches of 4
+#   rounds    - as filter, insertion budget 1: several filter/replay rounds
+#   rounds3   - budget 0 and 3 rounds: the last round filters with M
 MODES = {
     "default": {},
     "filter": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"},
     "overflow": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_POOL_PAGES": "2"},
     "subbatch": {"ICQ_PRO_MAX": "4096", "ICQ_PRO_MIN": "0", "ICQ_QBATCH": "4"},
+    # insertion budget 1: the replay stops after two insertions and the next
+    # round re-filters the rest (the third round filters with M, unbudgeted)
+    "rounds": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "1", "ICQ_ROUNDS": "8"},
+    "rounds3": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "0", "ICQ_ROUNDS": "3"},
 }
 
 

@@ -83,6 +83,7 @@ def main():
     ap.add_argument("--sigma", type=float, default=None)
     ap.add_argument("--n", type=int, default=0, help="truncate the database (0 = full)")
     ap.add_argument("--sweeps", type=int, default=10)
+    ap.add_argument("--only", type=str, default="", help="comma-separated query indices")
     args = ap.parse_args()
 
     import torch
@@ -103,7 +104,8 @@ def main():
     slow = torch.as_tensor([b for b in range(w.K) if b not in set(fast_books.tolist())],
                            device="cuda", dtype=torch.long)
     out = []
-    for qi in range(Q.shape[0]):
+    sel = [int(x) for x in args.only.split(",")] if args.only else list(range(Q.shape[0]))
+    for qi in sel:
         q = Q[qi]
         lut = ((B - q[None, None, :]) ** 2).sum(-1)  # (K, m)
         fast = torch.zeros(n, dtype=torch.float64, device="cuda")
