@@ -342,7 +342,7 @@ def main():
         "pruning": {"refined_fraction": float(refine.mean().item() / w.n),
                     "insertions_per_query": float(stats[:, 0].mean().item()),
                     "replay_live_candidates_per_query": float(stats[:, 1].mean().item()),
-                    "f64_certified_per_query": float(stats[:, 2].mean().item()),
+                    "filter_rounds_per_query": float(stats[:, 2].mean().item()),
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),
                     "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
                     "replay_cycles_per_query": float(stats[:, 5].mean().item()),
@@ -357,7 +357,7 @@ def main():
                         "prefilter": float(stats[:, 12].mean().item()),
                         "score": float(stats[:, 13].mean().item()),
                         "decide": float(stats[:, 14].mean().item()),
-                        "blocks": float(stats[:, 15].mean().item())},
+                        "serial_loop": float(stats[:, 15].mean().item())},
                     "recall_vs_exact": recall},
         "roofline": {"bound": "hbm", "achieved": filter_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": filter_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),

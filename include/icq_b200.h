@@ -99,11 +99,13 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
  *   refine_dev   : int64 [Q]     ops.refinements (search.py:160); may be NULL
  *   survivors_dev: optional uint32 bitmap [Q * ceil(n/32)] of refined ids
  *                  (instrumentation for parity tests; NULL to skip)
- *   stats_dev    : optional int64 [Q*16] diagnostics per query: heap insertions,
- *                  items examined by the in-order replay, items certified in
- *                  float64 (near-ties of the fp32 filter), end of the dense
- *                  prologue (item id), prologue cycles, phase-2 cycles,
- *                  replay cycles spent waiting for the scan, wide-mode flag
+ *   stats_dev    : optional int64 [Q*16] diagnostics per query (see
+ *                  paper_1912_08756_b200.search.STATS_NAMES): heap insertions,
+ *                  items decided by the replay, filter rounds, prologue end,
+ *                  prologue / replay cycles, rescanned slices (| overflow
+ *                  counts << 20 / << 40), wide flag, prologue float64 scorings,
+ *                  filter candidates, prologue insertions, filter threshold
+ *                  (float32 bits), prologue phase cycles
  *   fallback_out : optional host int32; set to 1 when the fast set is empty and
  *                  the exact engine ran instead (search.py:127-131)
  * The call is asynchronous on `stream` (no host synchronisation).

@@ -170,8 +170,9 @@ struct RepLayout {
   uint32_t lut64, lutf, he, hf, hi, wid, widx, wfv, wfe, meta, cum, chunks, ring, ringe, plist, ctl,
       total;
 };
-constexpr int kSG = 64;    // slices whose meta the replay stages in shared memory at once
+constexpr int kSG = 32;    // slices whose meta the replay stages in shared memory at once
 constexpr int kCH = 512;   // candidate entries per staged chunk (replay ring slot)
+constexpr int kRSlots = 4;  // replay ring: decide c | prepare c+1 | in flight c+2, c+3
 __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   RepLayout L;
   uint32_t o = 0;
@@ -187,8 +188,8 @@ __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   L.meta = o;  o = al16(o + kSG * kSliceInts * 4);
   L.cum = o;   o = al16(o + (kSG + 1) * 4);
   L.chunks = o; o = al16(o + 512 * 3 * 4);
-  L.ring = o;  o = al16(o + 3 * kCH * 16);
-  L.ringe = o; o = al16(o + 3 * kCH * 8);
+  L.ring = o;  o = al16(o + kRSlots * kCH * 16);
+  L.ringe = o; o = al16(o + kRSlots * kCH * 8);
   L.plist = o; o = al16(o + kCH * 4);
   L.ctl = o;   o = al16(o + 64);
   L.total = o;
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   int64_t pos = k;
   int64_t pro_cand = 0;
   long long tp[3] = {0, 0, 0};
+  long long t_loop = 0;  // thread 0: the serial decision loop alone
   int64_t nblocks = 0;
   int ins_hist[4] = {0, 0, 0, 0};  // thread 0: insertions of the last four blocks
   while (*flag) {
@@ -424,6 +426,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     //     the root is replaced and sifted down; bound = fast of the new root)
     if (tid == 0) {
       const int64_t ins_before = insertions;
+      const long long tl0 = clock64();
       const int64_t ins_limit = *pub_J >= kInfBudget ? INT64_MAX : insertions + *pub_J;
       *cut = -1;
       double T = he[0];
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
         }
         if (*cut >= 0) break;
       }
+      t_loop += clock64() - tl0;
       ins_hist[nblocks & 3] = (int)(insertions - ins_before);
       *ins_recent = ins_hist[0] + ins_hist[1] + ins_hist[2] + ins_hist[3];
     }
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     st.pro_t[0] = tp[0];
     st.pro_t[1] = tp[1];
     st.pro_t[2] = tp[2];
-    st.pro_t[3] = nblocks;
+    st.pro_t[3] = t_loop;  // (was: blocks)
     st.hi = fhi;
     st.lo = flo;
     st.thr = thr;
@@ -1014,7 +1018,6 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
 // published) and chunk c decided, all at once, one CTA barrier per chunk.
 constexpr int kRW = 4;            // warps per replay CTA
 constexpr int kRP = (kRW - 1) * 32;  // preparing threads
-constexpr int kRSlots = 3;
 constexpr int kMaxChunks = 512;   // chunk descriptors per slice group
 
 template <int FP>
@@ -1190,7 +1193,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
           ent.w = (uint32_t)(fb >> 32);
           src[i] = ent;
           ex[i] = __longlong_as_double(0x7ff8000000000000LL);
-          if (f < thr) plist[atomicAdd((int*)&ctl[2], 1)] = i;
+          if (f < thr && !(p.debug & 2)) plist[atomicAdd((int*)&ctl[2], 1)] = i;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
         const int nl = ctl[2];
@@ -1206,15 +1209,16 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
         issue(0);
         issue(1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        issue(2);
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
         prep(0);
       }
       __syncthreads();
       for (int ch = 0; ch < nc; ++ch) {
         if (warp > 0) {
-          issue(ch + 2);
-          asm volatile("cp.async.wait_group 1;" ::: "memory");  // chunk ch+1 landed
+          issue(ch + 3);
+          asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch+1 landed
           asm volatile("bar.sync 1, %0;" ::"n"(kRP));
           prep(ch + 1);
         } else if (chunk[3 * ch + 2] >= 0) {

@@ -78,7 +78,8 @@ struct PipeParams {
   int32_t range_major;        // filter unit order (L2 reuse of codes larger than L2)
   int32_t exact_mode;         // search_exact: report refinements = n (search.py:108)
   int32_t pro_div;            // prologue stops once a block's candidates <= items / pro_div
-  int32_t debug;              // experiments only (ICQ_DEBUG): bit 0 = no tuple-tie rejection
+  int32_t debug;              // experiments only (ICQ_DEBUG): bit 0 = no tuple-tie rejection,
+                              // bit 1 = replay producers skip exact scores
   int32_t round;              // current filter/replay round (0-based)
   int32_t j0;                 // first-round insertion budget (-1: from the insertion rate)
   int32_t max_rounds;         // filter/replay rounds (1: no insertion budgets, threshold M)

@@ -30,11 +30,11 @@ from .data import DeviceError, UnsupportedError, ValidationError
 
 # per-query int64 diagnostics written by the replay kernel (icq_b200.h stats_dev)
 STATS_FIELDS = 16
-STATS_NAMES = ("insertions", "replay_candidates", "f64_certified", "prologue_end",
+STATS_NAMES = ("insertions", "replay_candidates", "filter_rounds", "prologue_end",
                "prologue_cycles", "replay_cycles", "rescanned_slices", "wide",
                "prologue_f64_scored", "filter_candidates", "prologue_insertions",
                "filter_hi_f32_bits", "prologue_filter_cycles", "prologue_score_cycles",
-               "prologue_decide_cycles", "prologue_blocks")
+               "prologue_decide_cycles", "prologue_serial_loop_cycles")
 
 
 @dataclass
