@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "../../include/icq_b200.h"
-#include "icq_types.cuh"
+#include "icq_common.cuh"
 
 
 using namespace icq;
@@ -50,8 +50,8 @@ struct icq_index_s {
   int64_t n, n_pad;
   float* books;
   uint8_t* codes_full;
-  uint8_t* codes_fast;
-  bool fast_alias;
+  uint8_t* codes_fast;   // fast books, tile-transposed (streamed by the filter)
+  uint8_t* codes_xfull;  // all books, tile-transposed (the exact engine's stream)
   uint8_t fast_books[kMaxK];
   LutProg* prog_dev;
   int32_t* err_dev;
@@ -74,7 +74,8 @@ static int pow2_ceil(int x) {
 template <typename CodeT>
 __global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t n, int K, int m, int KP,
                               uint8_t* __restrict__ full, int FP, int F, const FastBooks fb,
-                              uint8_t* __restrict__ fastp, int32_t* err) {
+                              uint8_t* __restrict__ fastp, uint8_t* __restrict__ xfull,
+                              int32_t* err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint8_t row[kMaxK];
@@ -86,9 +87,14 @@ __global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t n, int K,
   }
   if (bad) atomicOr(err, 2);
   for (int b = 0; b < KP; ++b) full[i * KP + b] = b < K ? row[b] : 0;
+  // streamed rows in the tile-transposed layout (icq_common.cuh perm_chunk):
+  // the fast books, and all books for the exact engine
   if (fastp) {
-    for (int s = 0; s < FP; ++s) fastp[i * FP + s] = s < F ? row[fb.b[s]] : 0;
+    uint8_t* dst = fastp + perm_offset(FP, i);
+    for (int s = 0; s < FP; ++s) dst[s] = s < F ? row[fb.b[s]] : 0;
   }
+  uint8_t* xd = xfull + perm_offset(KP, i);
+  for (int b = 0; b < KP; ++b) xd[b] = b < K ? row[b] : 0;
 }
 
 template <typename CodeT>
@@ -125,29 +131,29 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
     h->fast_books[s] = (uint8_t)fast[s];
     prefix &= fast[s] == (uint32_t)s;
   }
-  h->fast_alias = F > 0 && prefix && h->FP == h->KP;
+  (void)prefix;
 
   auto cleanup = [&](icq_status st) {
     cudaFree(h->books); cudaFree(h->codes_full);
-    if (!h->fast_alias) cudaFree(h->codes_fast);
+    cudaFree(h->codes_fast); cudaFree(h->codes_xfull);
     cudaFree(h->prog_dev); cudaFree(h->err_dev);
     delete h;
     return st;
   };
   const size_t bbytes = (size_t)K * m * d * sizeof(float);
   const size_t fullb = (size_t)h->n_pad * h->KP;
-  const size_t fastb = (F && !h->fast_alias) ? (size_t)h->n_pad * h->FP : 0;
+  const size_t fastb = F ? (size_t)h->n_pad * h->FP : 0;
   cudaError_t e;
   if ((e = cudaMalloc(&h->books, bbytes)) != cudaSuccess ||
       (e = cudaMalloc(&h->codes_full, fullb)) != cudaSuccess ||
       (fastb && (e = cudaMalloc(&h->codes_fast, fastb)) != cudaSuccess) ||
+      (e = cudaMalloc(&h->codes_xfull, fullb)) != cudaSuccess ||
       (e = cudaMalloc(&h->prog_dev, sizeof(LutProg))) != cudaSuccess ||
       (e = cudaMalloc(&h->err_dev, sizeof(int32_t))) != cudaSuccess) {
     fail(ICQ_ERR_NOMEM, "device allocation failed: %s", cudaGetErrorString(e));
     return cleanup(ICQ_ERR_NOMEM);
   }
-  if (h->fast_alias) h->codes_fast = h->codes_full;
-  h->bytes = (int64_t)(bbytes + fullb + fastb);
+  h->bytes = (int64_t)(bbytes + 2 * fullb + fastb);
 
   const CodeT* codes_dev = codes;
   CodeT* staged = nullptr;
@@ -160,6 +166,7 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
     if ((e2 = cudaMemsetAsync(h->err_dev, 0, sizeof(int32_t), stream)) != cudaSuccess) return e2;
     if ((e2 = cudaMemsetAsync(h->codes_full, 0, fullb, stream)) != cudaSuccess) return e2;
     if (fastb && (e2 = cudaMemsetAsync(h->codes_fast, 0, fastb, stream)) != cudaSuccess) return e2;
+    if ((e2 = cudaMemsetAsync(h->codes_xfull, 0, fullb, stream)) != cudaSuccess) return e2;
     if (!on_device) {
       const size_t cb = (size_t)n * K * sizeof(CodeT);
       if ((e2 = cudaMalloc(&staged, cb)) != cudaSuccess) return e2;
@@ -174,7 +181,7 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
     const unsigned blocks = (unsigned)((n + threads - 1) / threads);
     repack_kernel<CodeT><<<blocks, threads, 0, stream>>>(
         codes_dev, n, K, m, h->KP, h->codes_full, h->FP, F, fb,
-        (F && !h->fast_alias) ? h->codes_fast : nullptr, h->err_dev);
+        F ? h->codes_fast : nullptr, h->codes_xfull, h->err_dev);
     if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
     return cudaStreamSynchronize(stream);
   };
@@ -250,7 +257,8 @@ icq_status icq_index_destroy(icq_index_t h) {
   if (!h) return ICQ_OK;
   cudaFree(h->books);
   cudaFree(h->codes_full);
-  if (!h->fast_alias) cudaFree(h->codes_fast);
+  cudaFree(h->codes_fast);
+  cudaFree(h->codes_xfull);
   cudaFree(h->prog_dev);
   cudaFree(h->err_dev);
   cudaFree(h->host_buf);
@@ -325,7 +333,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   p.exact_mode = exact ? 1 : 0;
   int FP;
   if (exact) {
-    p.codes_fast = h->codes_full;
+    p.codes_fast = h->codes_xfull;
     p.F = h->K;
     FP = h->KP;
     for (int b = 0; b < h->K; ++b) p.fast_books[b] = (uint8_t)b;

@@ -47,6 +47,38 @@ __device__ __forceinline__ Row load_row(const uint8_t* codes_full, int KP, int64
   return r;
 }
 
+// Tile-transposed layout of the streamed fast rows (codes_fast): within each
+// tile of 128 16-byte chunks, logical chunk lc = 4*lane + v is stored at
+// physical chunk 32*v + lane.  A coalesced warp load of chunks 32*v + lane
+// (v = 0..3) then hands every lane 4 CONSECUTIVE logical chunks, so a lane's
+// items form one contiguous id run (ordered compaction = one lane scan).
+__host__ __device__ inline int64_t perm_chunk(int64_t lc) {
+  return (lc & ~(int64_t)127) | ((lc & 3) << 5) | ((lc & 127) >> 2);
+}
+__host__ __device__ inline int64_t perm_offset(int FP, int64_t i) {  // byte offset of item i
+  const int ipc = 16 / FP;
+  return perm_chunk(i / ipc) * 16 + (i % ipc) * FP;
+}
+__device__ __forceinline__ Row load_fast_row(const uint8_t* codes_fast, int FP, int64_t i) {
+  Row r;
+  r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0;
+  const uint8_t* q = codes_fast + perm_offset(FP, i);
+  if (FP == 16) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(q));
+    r.w[0] = v.x; r.w[1] = v.y; r.w[2] = v.z; r.w[3] = v.w;
+  } else if (FP == 8) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(q));
+    r.w[0] = v.x; r.w[1] = v.y;
+  } else if (FP == 4) {
+    r.w[0] = __ldg(reinterpret_cast<const uint32_t*>(q));
+  } else if (FP == 2) {
+    r.w[0] = __ldg(reinterpret_cast<const uint16_t*>(q));
+  } else {
+    r.w[0] = __ldg(q);
+  }
+  return r;
+}
+
 __device__ __forceinline__ double exact64(const double* lut, int m, int K, bool pw, const Row& r) {
   return ref_row_sum(K, pw, [&](int b) { return lut[b * m + (int)r.byte(b)]; });
 }

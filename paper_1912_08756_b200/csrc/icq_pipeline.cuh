@@ -338,14 +338,17 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     const int64_t i0 = base + (int64_t)tid * 8;
     uint32_t w[2 * FP];
     {
-      const uint8_t* src = p.codes_fast + i0 * FP;
+      // 8 consecutive items = FP/2 logical chunks (half of one for FP == 1)
+      // of the tile-transposed fast rows
       if (FP == 1) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2*>(src));
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p.codes_fast + perm_offset(1, i0)));
         w[0] = v.x; w[1] = v.y;
       } else {
+        constexpr int kIpc = 16 / (FP > 1 ? FP : 1);
 #pragma unroll
         for (int t = 0; t < FP / 2; ++t) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + t);
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.codes_fast) +
+                                perm_chunk(i0 / kIpc + t));
           w[4 * t] = v.x; w[4 * t + 1] = v.y; w[4 * t + 2] = v.z; w[4 * t + 3] = v.w;
         }
       }
@@ -597,7 +600,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     const bool ok = ties && FP <= 8 && best >= 0;
     uint2 tup = make_uint2(0u, 0u);
     if (ok) {
-      const Row r = load_row(p.codes_fast, FP, hi[best]);
+      const Row r = load_fast_row(p.codes_fast, FP, hi[best]);
       tup = make_uint2(r.w[0], r.w[1]);
     }
     QState st;
@@ -684,6 +687,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
+  const uint32_t two = 2u + (uint32_t)(p.n < 0);    // 2, opaque to the compiler (keeps IMADs)
   int cur_q = -1;
   for (int64_t u = u0; u < u1; u += ustep) {
     const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
@@ -746,6 +750,10 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     };
     int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
     // 32-bit tile counters and a running chunk pointer (no 64-bit index math per tile)
+    // tile-transposed rows: the coalesced load of physical chunks 32 v + lane
+    // gives lane l the logical chunks 4 l .. 4 l + 3 of the tile, one
+    // contiguous id run, so an ordered append is a single lane scan
+    static_assert(V == 4, "the tile-transposed layout assumes 4 chunks per lane");
     const uint4* cptr = codes + t / IPC + lane;
     const int ntile = (int)((w_hi - t + TILE - 1) / TILE);
     uint4 a[V];
@@ -784,32 +792,38 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           f[v][j] = acc[0];
         }
       }
-      // (edge tiles: items outside [start, w_hi) are dropped from the
-      // candidate bits below; the cheap minimum test may fire spuriously there)
-      float lm = f[0][0];
-#pragma unroll
-      for (int v = 0; v < V; ++v)
-#pragma unroll
-        for (int j = 0; j < IPC; ++j) lm = fminf(lm, f[v][j]);
-      if (!__any_sync(kFull, lm < hi)) continue;
-      // ---- slow path (most tiles hold a candidate or two) ----
+      // candidate bits (bit v*IPC + j): x32 < hi.  Built on the FMA pipe (the
+      // ALU pipe carries the byte_perm address of every lookup): d = f - hi is
+      // negative iff f < hi, its sign bit is mul.hi(bits(d), 2), and the bits
+      // are accumulated Horner-style (acc = acc * 2 + s) with a runtime two.
+      // Items whose fast-code tuple is the threshold item's are dropped below
+      // (fast == thr exactly: never a candidate; few-codeword books make such
+      // ties common).  The kept set is a superset of the refined items; the
+      // replay decides exactly with the float64 score of the tuple.
       using Mask = typename std::conditional<(V * IPC > 32), unsigned long long, uint32_t>::type;
-      // candidate bits (bit v*IPC + j): x32 < hi, except the items whose
-      // fast-code tuple is the threshold item's (fast == thr exactly: never
-      // a candidate; few-codeword books make such ties common).  Everything
-      // kept is a superset of the refined items; the replay decides exactly
-      // with the float64 score of the tuple.
       Mask cm = 0;
+      if constexpr (V * IPC <= 32) {
+        uint32_t acc = 0;
 #pragma unroll
-      for (int v = 0; v < V; ++v)
+        for (int idx = V * IPC - 1; idx >= 0; --idx) {
+          const float dd = f[idx / IPC][idx % IPC] - hi;
+          acc = acc * two + __umulhi(__float_as_uint(dd), two);
+        }
+        cm = acc;
+      } else {
 #pragma unroll
-        for (int j = 0; j < IPC; ++j)
-          if (f[v][j] < hi) cm |= (Mask)1 << (v * IPC + j);
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int j = 0; j < IPC; ++j)
+            if (f[v][j] < hi) cm |= (Mask)1 << (v * IPC + j);
+      }
+      if (!__any_sync(kFull, cm != 0)) continue;
+      // ---- slow path (most tiles hold a candidate or two) ----
       if (t < start || t + TILE > w_hi) {  // edge tile: keep items in [start, w_hi)
         const int lo_t = (int)(start - t), hi_t = (int)min((int64_t)TILE, w_hi - t);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const int c0 = (v * 32 + lane) * IPC;  // first item of chunk v, relative to t
+          const int c0 = (lane * V + v) * IPC;  // first item of chunk v, relative to t
           const int a0 = min(max(lo_t - c0, 0), IPC), a1 = min(max(hi_t - c0, 0), IPC);
           const Mask keep = (a1 > a0) ? (((((Mask)1 << (a1 - a0)) - 1) << a0) << (v * IPC)) : (Mask)0;
           const Mask band = (((Mask)1 << IPC) - 1) << (v * IPC);
@@ -834,23 +848,16 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           }
         }
       }
-      // positions in item order (v, lane, j): per v, the (few) lanes holding
-      // candidates take consecutive runs
-      int mybase[V];
-      int g = cnt;
+      // positions: item order is (lane, v, j) -> one exclusive scan of the
+      // per-lane counts
+      const int mine = __popcll((unsigned long long)cm);
+      int incl = mine;
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int cv = __popcll((unsigned long long)((cm >> (v * IPC)) & (((Mask)1 << IPC) - 1)));
-        uint32_t lanes = __ballot_sync(kFull, cv > 0);
-        mybase[v] = 0;
-        while (lanes) {
-          const int l = __ffs(lanes) - 1;
-          lanes &= lanes - 1;
-          if (lane == l) mybase[v] = g;
-          g += __shfl_sync(kFull, cv, l);
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
       }
-      const int T = g - cnt;
+      const int T = __shfl_sync(kFull, incl, 31);
       if (T == 0) continue;
       const int need = (cnt + T + kPG - 1) / kPG - npages;
       int base_pg = 0;
@@ -870,18 +877,11 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         }
       }
       if (!overflow) {
-        int curv = -1, gg = 0;
+        int gg = cnt + incl - mine;
         while (cm) {
           const int idx = (int)__ffsll((unsigned long long)cm) - 1;
           cm &= cm - 1;
           const int v = idx / IPC, j = idx % IPC;
-          if (v != curv) {
-            curv = v;
-            gg = mybase[0];
-#pragma unroll
-            for (int vv = 1; vv < V; ++vv)
-              if (vv == v) gg = mybase[vv];
-          }
           const uint4 xv = xsel(v);
           uint2 tail;
           if constexpr (FP <= 8) {
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           }
           const int pi = gg / kPG;
           const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
-          const int64_t id = t + (int64_t)(v * 32 + lane) * IPC + j;
+          const int64_t id = t + (int64_t)(lane * V + v) * IPC + j;
           p.pool[(int64_t)pid * kPG + (gg % kPG)] = make_uint4((uint32_t)id, 0u, tail.x, tail.y);
           ++gg;
         }
@@ -1241,7 +1241,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
               t2[u] = make_uint2(0u, 0u);
               e2[u] = __longlong_as_double(0x7ff8000000000000LL);
               if (valid2[u]) {
-                const Row r2 = load_row(p.codes_fast, FP, i);
+                const Row r2 = load_fast_row(p.codes_fast, FP, i);
                 if constexpr (FP <= 8) {
                   t2[u] = make_uint2(r2.w[0], r2.w[1]);
                 } else {
@@ -1323,7 +1323,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       ns.thr = hf[best];
       certified_bounds(ns.thr, F, ns.lo, ns.hi);
       if (st.mt_valid) {
-        const Row r = load_row(p.codes_fast, FP, hi[best]);
+        const Row r = load_fast_row(p.codes_fast, FP, hi[best]);
         ns.mtup[0] = r.w[0];
         ns.mtup[1] = r.w[1];
       }
