@@ -36,6 +36,10 @@
 #pragma once
 #include <type_traits>
 
+#ifndef ICQ_PREFETCH_TILES
+#define ICQ_PREFETCH_TILES 0
+#endif
+
 #include "icq_common.cuh"
 
 namespace icq {
@@ -71,7 +75,7 @@ __device__ __forceinline__ uint2 chunk_tuple(const uint4& xv, int j) {
     const int bo = j * FP;
     const int wi = bo >> 2;
     uint32_t w = ((wi == 0) ? xv.x : (wi == 1) ? xv.y : (wi == 2) ? xv.z : xv.w) >> ((bo & 3) * 8);
-    if (FP < 4) w &= (1u << (8 * FP)) - 1u;
+    if constexpr (FP < 4) w &= (1u << (8 * FP)) - 1u;
     return make_uint2(w, 0u);
   }
   return j == 0 ? make_uint2(xv.x, xv.y) : make_uint2(xv.z, xv.w);  // FP == 8
@@ -648,7 +652,7 @@ struct FGeo {
   static constexpr int TILE = 32 * V * IPC;                      // items per warp tile
   static constexpr uint32_t kSmemEnd = kPage * (1 + P);          // absolute end of the pages
 };
-constexpr int kPrefetchTiles = 8;  // L2 bulk-prefetch distance (tiles)
+constexpr int kPrefetchTiles = ICQ_PREFETCH_TILES;  // L2 bulk-prefetch distance (tiles; 0 = off)
 
 template <int FP>
 __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_constant__ PipeParams p) {
@@ -679,6 +683,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   const int64_t U = (int64_t)p.Q * p.NR;
   int64_t u0, u1, ustep;
   const bool rmaj = p.range_major || p.round > 0;
+  const bool rmaj_stream = p.range_major != 0;
   if (rmaj) {  // all CTAs sweep the ranges together: codes reused in L2, and in later
                // rounds the few unfinished queries spread over all SMs
     u0 = blockIdx.x; u1 = U; ustep = gridDim.x;
@@ -693,8 +698,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
     const int r = rmaj ? (int)(u / p.Q) : (int)(u % p.NR);
     const int64_t P = p.qs[q].P;
-    const float hi = p.qs[q].hi, lo = p.qs[q].lo;
-    const double thr = p.qs[q].thr;
+    const float hi = p.qs[q].hi;
+    const double thr = p.qs[q].thr;  // (FP = 16 entries carry the float64 fast score)
+    (void)thr;
     const uint2 mtup = make_uint2(p.qs[q].mtup[0], p.qs[q].mtup[1]);
     const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
@@ -769,7 +775,10 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         for (int v = 0; v < V; ++v) a[v] = ldg_stream(cptr + v * 32);
       }
       // L2 bulk prefetch kPrefetchTiles ahead, 4 tiles per request
-      if (lane == 0 && (it & 3) == 0 && it + kPrefetchTiles + 4 <= ntile)
+      // (only for streams larger than L2: an L2-resident stream gains nothing
+      // and the issue slots are the scarce resource there)
+      if (kPrefetchTiles > 0 && rmaj_stream && lane == 0 && (it & 3) == 0 &&
+          it + kPrefetchTiles + 4 <= ntile)
         prefetch_l2_bulk(cptr - lane + (kPrefetchTiles - 1) * (TILE / IPC), 4 * TILE * FP);
       // one warp tile: 32 lanes x V 16-byte chunks, items (v, lane, j)
       float f[V][IPC];
