@@ -945,14 +945,13 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
   const uint32_t lt = (1u << lane) - 1u;
   for (;;) {
     const double thr = L.thr64;
-    const float hhi = L.hi;
     uint32_t lm[kWU];
     double d[kWU];
     int base[kWU];
     int tot = 0;
 #pragma unroll
     for (int u = 0; u < kWU; ++u) {
-      bool cand = valid[u] && (u * 32 + lane >= pos0) && f32[u] < hhi;
+      bool cand = valid[u] && (u * 32 + lane >= pos0);  // (f32 is -inf for every caller)
       d[u] = 0.0;
       if (cand) {
         d[u] = entry_f64<FP>(tail[u], lutf, c.m, c.F);
@@ -1000,7 +999,7 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
         const double nf = __shfl_sync(kFull, f64, first);
         const int32_t nid = __shfl_sync(kFull, id, first);
         L.H.replace_max(ne, nid, nf, lane);
-        live_update(L, c.F, c.sigma, false);
+        live_update64(L, c.sigma);  // (the replay never uses the float32 bounds)
         ++L.insertions;
         if (L.insertions > c.ins_limit) {  // budget spent: later lists may be incomplete
           if (lane == 0) *c.stop_pos = (int64_t)nid + 1;
@@ -1082,6 +1081,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
   L.H.hf = hf;
   L.H.hi = hi;
   int64_t fallback_slices = 0, listed = 0;
+  long long t_work = 0, t_wait = 0;  // warp 0: deciding vs waiting at the chunk barrier
   RCtx c;
   c.lut = lut;
   c.codes_full = p.codes_full;
@@ -1225,6 +1225,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       }
       __syncthreads();
       for (int ch = 0; ch < nc; ++ch) {
+        const long long tw0 = clock64();
         if (warp > 0) {
           issue(ch + 3);
           asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch+1 landed
@@ -1296,7 +1297,9 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
           }
           if (lane == 0) *pub_thr = L.thr64;
         }
+        const long long tw1 = clock64();
         __syncthreads();
+        if (warp == 0) { t_work += tw1 - tw0; t_wait += clock64() - tw1; }
         if (ctl[3]) break;  // insertion budget spent: the next round resumes at *stop_pos
       }
       if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1370,8 +1373,8 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       s[9] = listed;
       s[10] = st.insertions;
       s[11] = __float_as_int(st.hi);
-      s[12] = st.pro_t[0];
-      s[13] = st.pro_t[1];
+      s[12] = (p.debug & 4) ? t_work : st.pro_t[0];  // debug bit 2: replay warp-0 timers
+      s[13] = (p.debug & 4) ? t_wait : st.pro_t[1];
       s[14] = st.pro_t[2];
       s[15] = st.pro_t[3];
     }

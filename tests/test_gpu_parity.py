@@ -130,6 +130,27 @@ def test_random_vs_oracle_with_survivors(cfg, mode, monkeypatch):
             assert np.array_equal(out["scores"][i].cpu().numpy(), ref.scores)
 
 
+@pytest.mark.parametrize("mode", ["default", "filter"])
+def test_large_k_shared_memory_heap(mode, monkeypatch):
+    """k > 128: the replay's heap lives in shared memory (WarpHeap smem path)."""
+    for key, val in MODES[mode].items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(21)
+    books, codes, fast = _random_case(rng, 30000, 12, 8, 256, 2)
+    dev = icqb.DeviceIndex(books, codes, fast)
+    Q = rng.standard_normal((3, 12))
+    for k in (129, 500, 2048):
+        for sigma in (0.0, 3.0):
+            ids, scores, refine, _ = dev.search_host(Q, k, sigma, exact=False)
+            for i in range(Q.shape[0]):
+                ref = O.two_step(books, codes, fast, sigma, Q[i], k)
+                assert np.array_equal(ids[i], ref.ids), (mode, k, sigma, i)
+                assert np.array_equal(scores[i], ref.scores), (mode, k, sigma, i)
+                assert int(refine[i]) == ref.ops.refinements, (mode, k, sigma, i)
+    with pytest.raises(icqb.UnsupportedError):
+        dev.search_host(Q, 2049, 0.0, exact=False)
+
+
 def test_batch_invariance():
     rng = np.random.default_rng(3)
     books, codes, fast = _random_case(rng, 12000, 16, 8, 256, 2)
