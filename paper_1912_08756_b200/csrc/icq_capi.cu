@@ -380,6 +380,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   {
     // insertion-budgeted filter rounds (experimental; 1 = one round with M)
     int64_t r = env_i("ICQ_ROUNDS", 1);
+    const char* sl = getenv("ICQ_BUDGET_SLACK");
+    p.budget_slack = sl ? atof(sl) : 0.05;
     p.max_rounds = (int32_t)(r < 1 ? 1 : (r > kRounds ? kRounds : r));
   }
   p.pro_min = env_i("ICQ_PRO_MIN", 8192);

@@ -244,6 +244,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   volatile int* ins_recent = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 100);  // last 4 blocks
   volatile int* pub_J = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 104);  // prefilter budget
   volatile long long* cut = reinterpret_cast<volatile long long*>(dsm + Ly.ctrl + 112);  // pass end
+  volatile float* pub_hiM = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 120);  // M's float32 hi
+  volatile int* final_J = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 124);      // budget at stop
+  int* nM_total = reinterpret_cast<int*>(dsm + Ly.ctrl + 92);  // block items under M (stop rule)
   const long long t0 = clock64();
 
   // 1. float64 LUT -> smem, float32 copy of the fast books (prefilter)
@@ -320,6 +323,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       *ins_recent = 0;
       *pub_J = kInfBudget;
       *cut = -1;
+      *pub_hiM = t.hi;
+      *final_J = kInfBudget;
+      *nM_total = 0;
     }
   }
   __syncthreads();
@@ -338,6 +344,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     const int64_t bend = min(n, base + kProBlock);
     const float h = *pub_hi, hl = *pub_lo;
     const double hthr = *pub_thr;
+    const float hM = *pub_hiM;
     // 3a. fp32 prefilter of 8 consecutive items per thread (codes_fast rows)
     const int64_t i0 = base + (int64_t)tid * 8;
     uint32_t w[2 * FP];
@@ -359,6 +366,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     }
     uint32_t mask = 0;
     int nband = 0;  // items float32 could not decide (near / exact ties with the threshold)
+    int nm = 0;     // items under M's float32 bound (how loose the unbudgeted filter would be)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float x = 0.f;
@@ -382,9 +390,11 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
         cand = d < hthr;
       }
       mask |= ((i >= pos) & (i < bend) & cand) ? (1u << j) : 0u;
+      nm += (i >= pos) & (i < bend) & (x < hM);
     }
     // 3b. ordered compaction (thread order = item order)
     if (nband) atomicAdd(band_total, nband);
+    if (nm) atomicAdd(nM_total, nm);
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll
@@ -500,6 +510,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     __syncwarp();
     if (warp == 0) {
       StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
+      const float hiM_next = tn.hi;  // M's bound for the next block's count
       // insertions have become rare: prefilter (and later filter) with the
       // budgeted A_J (max fast over the J+1 largest-exact entries), far
       // tighter than M when a high-fast item sits deep in the heap
@@ -507,7 +518,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       int Jpub = kInfBudget;
       if (p.max_rounds > 1 && p.sigma == 0.0 && !wide && nblocks >= 4 && Jc < kSelectJ &&
           Jc < k - 1) {
-        double A = -__longlong_as_double(0x7ff0000000000000LL);
+        double A = -__longlong_as_double(0x7ff0000000000000LL), A0 = 0.0;
         double pe = __longlong_as_double(0x7ff0000000000000LL);
         int32_t pi = 0x7fffffff;
         int Jt = 0;
@@ -528,6 +539,8 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
           }
           pe = be;
           pi = bi;
+          if (r == 0) A0 = bf;
+          else if (fmax(A, bf) > A0 * (1.0 + p.budget_slack)) break;  // stay near the live bound
           A = fmax(A, bf);
           Jt = r;
         }
@@ -541,9 +554,20 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       const int64_t pend = stopped ? (int64_t)*cut : bend;
       const int64_t nb = pend - max(pos, base);
       bool more = pend < n && pend < p.pro_max;
-      if (!stopped && bend >= p.pro_min && (int64_t)ncand * p.pro_div <= nb) more = false;
+      // stop once the filter's threshold passes <= 1/pro_div of a block: M
+      // itself (unbudgeted), or the budgeted A_J the prefilter just used
+      const bool under_budget = *pub_J < kInfBudget;  // this block's prefilter threshold
+      int fj = kInfBudget;  // budget the filter gets (also when the length cap ends it)
+      if (under_budget) fj = *pub_J;
+      if (!stopped && bend >= p.pro_min) {
+        if ((int64_t)(*nM_total) * p.pro_div <= nb) { more = false; fj = kInfBudget; }
+        else if (under_budget && (int64_t)ncand * p.pro_div <= nb) more = false;
+      }
       if (lane == 0) {
         *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *pub_J = Jpub;
+        *pub_hiM = hiM_next;
+        *final_J = fj;
+        *nM_total = 0;
         *flag = more ? 1 : 0;
       }
     }
@@ -579,9 +603,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     // insertion rate it is far tighter than M = A_{k-1} when a high-fast item
     // sits deep in the heap.  The replay stops when the budget runs out and
     // the next round re-filters the rest.  sigma > 0: U + sigma, unbudgeted.
-    const int rate = *ins_recent;
-    int J = p.j0 >= 0 ? p.j0 : rate * 2;
-    if (p.j0 < 0 && *pub_J >= kInfBudget) J = kInfBudget;  // M was the tighter threshold
+    int J = p.j0 >= 0 ? p.j0 : *final_J;  // the budget the prologue stopped under (M: none)
     int best = -1;
     double thr = *pub_thr;
     float flo = *pub_lo, fhi = *pub_hi;
@@ -1329,8 +1351,13 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       if (J >= k - 1) J = kInfBudget;
       const int top = J == kInfBudget ? k : J + 1;
       int best = 0;
-      for (int i = 1; i < top; ++i)
+      for (int i = 1; i < top; ++i) {
+        if (J != kInfBudget && p.j0 < 0 && hf[i] > hf[0] * (1.0 + p.budget_slack)) {
+          J = i - 1;  // stay near the live bound: grow the budget only while A_j does
+          break;
+        }
         if (hf[i] > hf[best]) best = i;
+      }
       ns.J = J;
       ns.thr = hf[best];
       certified_bounds(ns.thr, F, ns.lo, ns.hi);

@@ -39,7 +39,7 @@ struct QState {
   int32_t rounds;       // filter/replay rounds used
 };
 constexpr int32_t kInfBudget = 1 << 30;
-constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)
+constexpr int kRounds = 16;  // filter/replay rounds (the last one filters with M: no budget)
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries)
@@ -83,6 +83,7 @@ struct PipeParams {
   int32_t round;              // current filter/replay round (0-based)
   int32_t j0;                 // first-round insertion budget (-1: from the insertion rate)
   int32_t max_rounds;         // filter/replay rounds (1: no insertion budgets, threshold M)
+  double budget_slack;        // A_J may exceed the live bound A_0 by this relative margin
   int64_t pro_min, pro_max;   // prologue length bounds (items)
   uint8_t fast_books[kMaxK];
 };
