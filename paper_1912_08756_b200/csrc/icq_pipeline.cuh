@@ -560,7 +560,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       int fj = kInfBudget;  // budget the filter gets (also when the length cap ends it)
       if (under_budget) fj = *pub_J;
       if (!stopped && bend >= p.pro_min) {
-        if ((int64_t)(*nM_total) * p.pro_div <= nb) { more = false; fj = kInfBudget; }
+        // (under M the prefilter count is exact: near-ties were resolved in float64)
+        const int64_t nM = under_budget ? (int64_t)(*nM_total) : (int64_t)ncand;
+        if (nM * p.pro_div <= nb) { more = false; fj = kInfBudget; }
         else if (under_budget && (int64_t)ncand * p.pro_div <= nb) more = false;
       }
       if (lane == 0) {
