@@ -562,8 +562,12 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       if (!stopped && bend >= p.pro_min) {
         // (under M the prefilter count is exact: near-ties were resolved in float64)
         const int64_t nM = under_budget ? (int64_t)(*nM_total) : (int64_t)ncand;
-        if (nM * p.pro_div <= nb) { more = false; fj = kInfBudget; }
-        else if (under_budget && (int64_t)ncand * p.pro_div <= nb) more = false;
+        if (nM * p.pro_div <= nb) {
+          more = false;
+          fj = kInfBudget;
+        } else if (under_budget && (int64_t)ncand * p.pro_div <= nb && nM * p.pro_div > 16 * nb) {
+          more = false;  // M is grossly loose, the budgeted A_J is not: rounds pay off
+        }
       }
       if (lane == 0) {
         *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *pub_J = Jpub;
@@ -1348,8 +1352,9 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       ns.refinements = L.refinements;
       ns.insertions = L.insertions;
       ns.ins0 = L.insertions;
-      int J = (p.round + 2 >= p.max_rounds || st.J >= kInfBudget / 4) ? kInfBudget
-                                                                       : max(4, 2 * (st.J + 1));
+      // next budget: as many insertions as A_j stays near the live bound
+      // (recomputed from the heap; the last round is unbudgeted)
+      int J = (p.round + 2 >= p.max_rounds || st.J >= kInfBudget) ? kInfBudget : kSelectJ;
       if (J >= k - 1) J = kInfBudget;
       const int top = J == kInfBudget ? k : J + 1;
       int best = 0;

@@ -39,7 +39,7 @@ struct QState {
   int32_t rounds;       // filter/replay rounds used
 };
 constexpr int32_t kInfBudget = 1 << 30;
-constexpr int kRounds = 16;  // filter/replay rounds (the last one filters with M: no budget)
+constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries)
