@@ -181,32 +181,6 @@ struct WarpHeap {
   }
   __device__ __forceinline__ double top_e() const { return ue[0]; }
   __device__ __forceinline__ double top_f() const { return uf[0]; }
-  // largest fast score over the whole heap (warp-uniform result)
-  __device__ __forceinline__ double max_fast_all(int lane) const {
-    double a = -__longlong_as_double(0x7ff0000000000000LL);
-    if (reg) {
-#pragma unroll
-      for (int r = 0; r < kRegHeapRegs; ++r)
-        if (kRegHeapRegs * lane + r < k) a = fmax(a, f[r]);
-    } else {
-      for (int i = lane; i < k; i += 32) a = fmax(a, hf[i]);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    return a;
-  }
-  // true when some heap fast score is NaN (fmax would hide it)
-  __device__ __forceinline__ bool any_nan_fast(int lane) const {
-    bool bad = false;
-    if (reg) {
-#pragma unroll
-      for (int r = 0; r < kRegHeapRegs; ++r)
-        if (kRegHeapRegs * lane + r < k) bad |= !(f[r] == f[r]);
-    } else {
-      for (int i = lane; i < k; i += 32) bad |= !(hf[i] == hf[i]);
-    }
-    return __any_sync(0xffffffffu, bad);
-  }
   __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
     // 1. uniform top cache: drop entry 0, insert x if it ranks inside the prefix
     double le = ue[0];
@@ -313,13 +287,7 @@ __device__ __forceinline__ StaleThr stale_core(double M, bool nan, double T, int
   certified_bounds(thr, F, r.lo, r.hi);
   return r;
 }
-__device__ __forceinline__ StaleThr stale_filter(const Live& L, int F, double sigma, double smin,
-                                                 bool wide, int lane) {
-  const double M = L.H.max_fast_all(lane);
-  const bool nan = L.H.any_nan_fast(lane);
-  return stale_core(M, nan, L.T64, F, sigma, smin, wide);
-}
-// same, from a heap array in shared memory (any order; entry 0 = maximum), one warp
+// stale threshold from a heap array in shared memory (any order; entry 0 = maximum), one warp
 __device__ __forceinline__ StaleThr stale_from_heap(const double* he, const double* hf, int k,
                                                     int F, double sigma, double smin, bool wide,
                                                     int lane) {

@@ -94,58 +94,6 @@ __device__ __forceinline__ double tuple_f64(uint2 t, const double* lut64f, int m
   return d;
 }
 
-// One decision round over up to 32 items in database order (lane order):
-// search.py:149-154 applied until the first insertion.
-__device__ __forceinline__ Decided decide_round(Live& L, const RCtx& c, int lane, bool cand,
-                                                float fv, int32_t id, bool& have, double& f64,
-                                                double& e64) {
-  const uint32_t cmask = __ballot_sync(kFull, cand);
-  Decided d{-1, kFull};
-  if (!cmask) return d;
-  bool refined = false, certified = false;
-  if (cand) {
-    if (!c.wide && fv < L.lo) {
-      refined = true;
-    } else {
-      if (!have) {
-        const Row r = load_row(c.codes_full, c.KP, id);
-        f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
-        e64 = exact64(c.lut, c.m, c.K, c.pw, r);
-        have = true;
-      }
-      certified = true;
-      refined = f64 < L.thr64;
-    }
-    if (refined && !have) {
-      const Row r = load_row(c.codes_full, c.KP, id);
-      f64 = fast64(c.lut, c.m, c.F, c.pw, c.fb, r);
-      e64 = exact64(c.lut, c.m, c.K, c.pw, r);
-      have = true;
-    }
-  }
-  const bool ins = refined && (e64 < L.T64);
-  const uint32_t rmask = __ballot_sync(kFull, refined);
-  const uint32_t imask = __ballot_sync(kFull, ins);
-  const uint32_t cert = __ballot_sync(kFull, certified);
-  const int first = imask ? __ffs(imask) - 1 : 31;
-  const uint32_t decided = imask ? (kFull >> (31 - first)) : kFull;
-  L.refinements += __popc(rmask & decided);
-  L.candidates += __popc(cmask & decided);
-  L.certified += __popc(cert & decided);
-  if (refined && ((decided >> lane) & 1u)) record_survivor(c.surv, id);
-  d.done = decided;
-  if (imask) {
-    d.first = first;
-    const double ne = __shfl_sync(kFull, e64, first);
-    const double nf = __shfl_sync(kFull, f64, first);
-    const int32_t nid = __shfl_sync(kFull, id, first);
-    L.H.replace_max(ne, nid, nf, lane);
-    live_update(L, c.F, c.sigma, c.wide);
-    ++L.insertions;
-  }
-  return d;
-}
-
 // --------------------------------------------------------------------------
 // shared-memory layouts
 // --------------------------------------------------------------------------
