@@ -67,6 +67,12 @@ struct Decided {
   uint32_t done;  // lanes decided in this round
 };
 
+__device__ __forceinline__ uint32_t sel_u32(int c, uint32_t a, uint32_t b) {  // c ? a : b
+  uint32_t r;
+  asm("{ .reg .pred p; setp.ne.s32 p, %1, 0; selp.b32 %0, %2, %3, p; }" : "=r"(r) : "r"(c), "r"(a), "r"(b));
+  return r;
+}
+
 // Fast-code tuple of item j of a 16-byte chunk (FP <= 8 bytes, little-endian
 // in .x/.y); runtime j selects words, no dynamically indexed arrays.
 template <int FP>
@@ -74,7 +80,9 @@ __device__ __forceinline__ uint2 chunk_tuple(const uint4& xv, int j) {
   if (FP <= 4) {
     const int bo = j * FP;
     const int wi = bo >> 2;
-    uint32_t w = ((wi == 0) ? xv.x : (wi == 1) ? xv.y : (wi == 2) ? xv.z : xv.w) >> ((bo & 3) * 8);
+    // three selects on the bits of wi (no branches in the candidate loops)
+    const uint32_t lo = sel_u32(wi & 1, xv.y, xv.x), hi = sel_u32(wi & 1, xv.w, xv.z);
+    uint32_t w = sel_u32(wi & 2, hi, lo) >> ((bo & 3) * 8);
     if constexpr (FP < 4) w &= (1u << (8 * FP)) - 1u;
     return make_uint2(w, 0u);
   }
@@ -669,6 +677,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
   const uint32_t two = 2u + (uint32_t)(p.n < 0);    // 2, opaque to the compiler (keeps IMADs)
+  const uint32_t lt_mask = (1u << lane) - 1u;
   int cur_q = -1;
   for (int64_t u = u0; u < u1; u += ustep) {
     const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
@@ -738,6 +747,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     static_assert(V == 4, "the tile-transposed layout assumes 4 chunks per lane");
     const uint4* cptr = codes + t / IPC + lane;
     const int ntile = (int)((w_hi - t + TILE - 1) / TILE);
+    // tiles [it_full0, it_full1) lie wholly inside [start, w_hi)
+    const int it_full0 = t < start ? 1 : 0;
+    const int it_full1 = t + (int64_t)ntile * TILE > w_hi ? ntile - 1 : ntile;
     uint4 a[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) a[v] = ldg_stream(cptr + v * 32);
@@ -756,55 +768,73 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       if (kPrefetchTiles > 0 && rmaj_stream && lane == 0 && (it & 3) == 0 &&
           it + kPrefetchTiles + 4 <= ntile)
         prefetch_l2_bulk(cptr - lane + (kPrefetchTiles - 1) * (TILE / IPC), 4 * TILE * FP);
-      // one warp tile: 32 lanes x V 16-byte chunks, items (v, lane, j)
-      float f[V][IPC];
+      // one warp tile: 32 lanes x V 16-byte chunks, items (v, lane, j).  The
+      // fast sums of item pairs run packed (FADD2: two fp32 adds per issue,
+      // each rounded as the scalar add, denormals kept), in the same tree order
+      // the certified bounds assume; d = f - hi keeps the sign of f - hi
+      // exactly (no flush), so d < 0 iff f < hi.
+      constexpr int N = V * IPC;
+      const float2 nhi2 = make_float2(-hi, -hi);
+      float2 d2[N / 2];
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+      for (int pr = 0; pr < N / 2; ++pr) {
+        float2 acc[FP];
 #pragma unroll
-        for (int j = 0; j < IPC; ++j) {
-          float acc[FP];
+        for (int h = 0; h < 2; ++h) {
+          const int idx = 2 * pr + h, v = idx / IPC, j = idx % IPC;
+          const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
 #pragma unroll
           for (int s = 0; s < FP; ++s) {
             const int byte = j * FP + s;
             const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
-            acc[s] = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
+            const float val = lds_f32(__byte_perm(wd[byte >> 2], Lp[s], sel));
+            if (h == 0) acc[s].x = val; else acc[s].y = val;
           }
-#pragma unroll
-          for (int h = 1; h < FP; h *= 2)
-#pragma unroll
-            for (int s = 0; s + h < FP; s += 2 * h) acc[s] = acc[s] + acc[s + h];
-          f[v][j] = acc[0];
         }
+#pragma unroll
+        for (int h = 1; h < FP; h *= 2)
+#pragma unroll
+          for (int s = 0; s + h < FP; s += 2 * h) acc[s] = __fadd2_rn(acc[s], acc[s + h]);
+        d2[pr] = __fadd2_rn(acc[0], nhi2);
       }
-      // candidate bits (bit v*IPC + j): x32 < hi.  Built on the FMA pipe (the
-      // ALU pipe carries the byte_perm address of every lookup): d = f - hi is
-      // negative iff f < hi, its sign bit is mul.hi(bits(d), 2), and the bits
-      // are accumulated Horner-style (acc = acc * 2 + s) with a runtime two.
-      // Items whose fast-code tuple is the threshold item's are dropped below
-      // (fast == thr exactly: never a candidate; few-codeword books make such
-      // ties common).  The kept set is a superset of the refined items; the
-      // replay decides exactly with the float64 score of the tuple.
-      using Mask = typename std::conditional<(V * IPC > 32), unsigned long long, uint32_t>::type;
+      // candidate bits (bit v*IPC + j): d < 0.  Built on the FMA pipe (the
+      // ALU pipe carries the byte_perm address of every lookup): the sign bit
+      // of d is mul.hi(bits(d), 2), accumulated Horner-style (acc = acc * 2 +
+      // s) with a runtime two.  Items whose fast-code tuple is the threshold
+      // item's are dropped below (fast == thr exactly: never a candidate;
+      // few-codeword books make such ties common).  The kept set is a
+      // superset of the refined items; the replay decides exactly with the
+      // float64 score of the tuple.
+      using Mask = typename std::conditional<(N > 32), unsigned long long, uint32_t>::type;
       Mask cm = 0;
-      if constexpr (V * IPC <= 32) {
-        uint32_t acc = 0;
+      if constexpr (N <= 32) {
+        // four independent Horner chains (short dependency paths), then merged
+        constexpr int NC = N >= 16 ? 4 : 1, L = N / NC;
+        uint32_t acc[NC];
 #pragma unroll
-        for (int idx = V * IPC - 1; idx >= 0; --idx) {
-          const float dd = f[idx / IPC][idx % IPC] - hi;
-          acc = acc * two + __umulhi(__float_as_uint(dd), two);
+        for (int c = 0; c < NC; ++c) {
+          acc[c] = 0;
+#pragma unroll
+          for (int i = L - 1; i >= 0; --i) {
+            const int idx = c * L + i;
+            const float dd = (idx & 1) ? d2[idx >> 1].y : d2[idx >> 1].x;
+            acc[c] = acc[c] * two + __umulhi(__float_as_uint(dd), two);
+          }
         }
-        cm = acc;
+        uint32_t mk = acc[0];
+#pragma unroll
+        for (int c = 1; c < NC; ++c) mk |= acc[c] << (c * L);
+        cm = mk;
       } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v)
-#pragma unroll
-          for (int j = 0; j < IPC; ++j)
-            if (f[v][j] < hi) cm |= (Mask)1 << (v * IPC + j);
+        for (int idx = 0; idx < N; ++idx) {
+          const float dd = (idx & 1) ? d2[idx >> 1].y : d2[idx >> 1].x;
+          if (dd < 0.f) cm |= (Mask)1 << idx;
+        }
       }
       if (!__any_sync(kFull, cm != 0)) continue;
       // ---- slow path (most tiles hold a candidate or two) ----
-      if (t < start || t + TILE > w_hi) {  // edge tile: keep items in [start, w_hi)
+      if (it < it_full0 || it >= it_full1) {  // edge tile: keep items in [start, w_hi)
         const int lo_t = (int)(start - t), hi_t = (int)min((int64_t)TILE, w_hi - t);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
@@ -815,34 +845,39 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           cm &= ~band | keep;
         }
       }
-      auto xsel = [&](int v) {
-        uint4 r = x[0];
-#pragma unroll
-        for (int vv = 1; vv < V; ++vv)
-          if (v == vv) r = x[vv];
-        return r;
-      };
+      constexpr uint32_t kChunkBits = IPC >= 32 ? 0xffffffffu : ((1u << IPC) - 1u);
       if constexpr (FP <= 8) {
         if (mt_valid) {  // lane-parallel tie check over the few candidate bits
-          Mask mm = cm;
-          while (mm) {
-            const int idx = (int)__ffsll((unsigned long long)mm) - 1;
-            mm &= mm - 1;
-            const uint2 tj = chunk_tuple<FP>(xsel(idx / IPC), idx % IPC);
-            if (tj.x == mtup.x && tj.y == mtup.y) cm &= ~((Mask)1 << idx);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            uint32_t b = (uint32_t)(cm >> (v * IPC)) & kChunkBits;
+            while (b) {
+              const int j = __ffs(b) - 1;
+              b &= b - 1;
+              const uint2 tj = chunk_tuple<FP>(x[v], j);
+              if (tj.x == mtup.x && tj.y == mtup.y) cm &= ~((Mask)1 << (v * IPC + j));
+            }
           }
         }
       }
-      // positions: item order is (lane, v, j) -> one exclusive scan of the
-      // per-lane counts
+      // positions: item order is (lane, v, j) -> an exclusive scan of the
+      // per-lane counts; one ballot when no lane holds two
       const int mine = __popcll((unsigned long long)cm);
-      int incl = mine;
+      const uint32_t has = __ballot_sync(kFull, mine != 0);
+      int excl, T;
+      if (!__any_sync(kFull, mine > 1)) {
+        excl = __popc(has & lt_mask);
+        T = __popc(has);
+      } else {
+        int incl = mine;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += y;
+        }
+        excl = incl - mine;
+        T = __shfl_sync(kFull, incl, 31);
       }
-      const int T = __shfl_sync(kFull, incl, 31);
       if (T == 0) continue;
       const int need = (cnt + T + kPG - 1) / kPG - npages;
       int base_pg = 0;
@@ -862,24 +897,28 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         }
       }
       if (!overflow) {
-        int gg = cnt + incl - mine;
-        while (cm) {
-          const int idx = (int)__ffsll((unsigned long long)cm) - 1;
-          cm &= cm - 1;
-          const int v = idx / IPC, j = idx % IPC;
-          const uint4 xv = xsel(v);
-          uint2 tail;
-          if constexpr (FP <= 8) {
-            tail = chunk_tuple<FP>(xv, j);
-          } else {
-            const unsigned long long db = (unsigned long long)__double_as_longlong(fast_f64(xv, j));
-            tail = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+        int gg = cnt + excl;
+        // ids fit 32 bits (n < 2^31); chunk v of this lane starts at idb + v*IPC
+        const uint32_t idb = (uint32_t)t + (uint32_t)(lane * N);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          uint32_t b = (uint32_t)(cm >> (v * IPC)) & kChunkBits;
+          while (b) {
+            const int j = __ffs(b) - 1;
+            b &= b - 1;
+            uint2 tail;
+            if constexpr (FP <= 8) {
+              tail = chunk_tuple<FP>(x[v], j);
+            } else {
+              const unsigned long long db = (unsigned long long)__double_as_longlong(fast_f64(x[v], j));
+              tail = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+            }
+            const int pi = gg >> 7;
+            const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
+            p.pool[((size_t)(uint32_t)pid << 7) | (uint32_t)(gg & (kPG - 1))] =
+                make_uint4(idb + (uint32_t)(v * IPC + j), 0u, tail.x, tail.y);
+            ++gg;
           }
-          const int pi = gg / kPG;
-          const int pid = pi < npages ? cur_page : base_pg + (pi - npages);
-          const int64_t id = t + (int64_t)(lane * V + v) * IPC + j;
-          p.pool[(int64_t)pid * kPG + (gg % kPG)] = make_uint4((uint32_t)id, 0u, tail.x, tail.y);
-          ++gg;
         }
         if (need > 0) {
           npages += need;

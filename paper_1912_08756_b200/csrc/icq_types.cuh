@@ -42,7 +42,7 @@ constexpr int32_t kInfBudget = 1 << 30;
 constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
-constexpr int kPG = 128;         // candidate pool page (entries)
+constexpr int kPG = 128;         // candidate pool page (entries; the filter indexes by gg >> 7)
 constexpr int kMaxPages = 64;    // pages per slice (more -> the replay rescans the slice)
 constexpr int kSliceInts = 4 + kMaxPages;  // count, 3 pad, page ids (16-byte rows)
 constexpr int kProThreads = 256;
