@@ -73,6 +73,8 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._proc = None
+        self.recording = False  # rows are kept only while the timed region runs
+        self._first = threading.Event()
 
     def __enter__(self):
         try:
@@ -88,7 +90,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self._proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self._first.set()
+            if self.recording:
+                self.rows.append([x.strip() for x in line.split(",")])
+
+    def wait_started(self, timeout=10.0):
+        """nvidia-smi is started before the warm-up (its start-up stalls the
+        driver); wait for its first sample so that happens outside timing."""
+        if self._proc is not None:
+            self._first.wait(timeout)
 
     def __exit__(self, *exc):
         if self._proc is not None:
@@ -221,6 +231,8 @@ def main():
             ev[2].record(stream)
         return qb.shape[0], out
 
+    clk = ClockSampler(local).__enter__()
+    clk.wait_started()
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -232,10 +244,12 @@ def main():
     L = icqb._native.lib()
     L.icq_profile_read(None, None)  # drop anything recorded during warm-up
     L.icq_profile_enable(1)  # CUDA events around each pipeline kernel, launch stream
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            outs.append(step(args.warmup + i, evs[i]))
-        torch.cuda.synchronize()
+    clk.recording = True
+    for i in range(args.steps):
+        outs.append(step(args.warmup + i, evs[i]))
+    torch.cuda.synchronize()
+    clk.recording = False
+    clk.__exit__(None, None, None)
     L.icq_profile_enable(0)
     import ctypes as _C
 
@@ -246,6 +260,7 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    step_ms = sorted(e[0].elapsed_time(e[2]) for e in evs)
     t_lut = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3
     t_scan = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3
     t_total = t_lut + t_scan
@@ -338,6 +353,7 @@ def main():
         "config": base_config,
         "glookups_per_s": nq_all * w.n * w.F / t_total / 1e9,
         "lut_ms_per_step": t_lut / args.steps * 1e3,
+        "step_ms_median_max": [step_ms[len(step_ms) // 2], step_ms[-1]],
         "scan_ms_per_step": t_scan / args.steps * 1e3,
         "pruning": {"refined_fraction": float(refine.mean().item() / w.n),
                     "insertions_per_query": float(stats[:, 0].mean().item()),

@@ -374,7 +374,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
   }
-  p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 256);
+  p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 512);
   p.debug = (int32_t)env_i("ICQ_DEBUG", 0);  // experiments only; results stay exact
   p.j0 = (int32_t)env_i("ICQ_J0", -1);        // tests: force the first-round insertion budget
   {
