@@ -280,7 +280,10 @@ def main():
     lookups = nq * w.n * w.F
     # the filter kernel streams the fast codes of items [P, n) of every query
     p_mean = float(stats[:, 3].mean().item())
-    filter_bytes = nq * (w.n - p_mean) * w.F
+    # items the filter streamed: after the prologue, minus the tails of slices
+    # that overflowed their candidate pages (the replay rescans those instead)
+    skipped = float(stats[:, 15].sum().item())
+    filter_bytes = (nq * (w.n - p_mean) - skipped) * w.F
     filter_gbs = filter_bytes / t_filter_k / 1e9  # per-GPU filter kernel (this rank)
     hbm_peak, sm_max, peak_kind = _peaks()
     smem_peak_glps = 148 * 32 * sm_max * 1e6 / 1e9
@@ -368,6 +371,7 @@ def main():
                     "wide_queries": int(stats[:, 7].sum().item()),
                     "prologue_f64_scored_per_query": float(stats[:, 8].mean().item()),
                     "filter_candidates_per_query": float(stats[:, 9].mean().item()),
+                    "filter_skipped_items_per_query": float(stats[:, 15].mean().item()),
                     "filter_pass_fraction": float(stats[:, 9].mean().item() / w.n),
                     "prologue_phase_cycles_per_query": {
                         "prefilter": float(stats[:, 12].mean().item()),

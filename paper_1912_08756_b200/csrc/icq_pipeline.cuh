@@ -266,8 +266,6 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
   __syncthreads();
 
-  // the heap: a binary max-heap by (exact, id) in shared memory (the sorted
-  // seed array is one); thread 0 applies the reference loop serially
   int64_t refinements = 0, insertions = 0;
   double smin = 0.0;
   if (warp == 0) {
@@ -286,11 +284,20 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
   __syncthreads();
 
+  // the heap: the seeds' sorted array, held by warp 0 as a WarpHeap
+  // (registers for k <= 128, else the shared-memory array itself)
+  WarpHeap H;
+  H.k = k;
+  H.reg = k <= 32 * kRegHeapRegs;
+  H.he = he;
+  H.hf = hf;
+  H.hi = hi;
+  if (warp == 0) H.load(lane);
+
   // 3. blocks of kProBlock items in database order
   int64_t pos = k;
   int64_t pro_cand = 0;
   long long tp[3] = {0, 0, 0};
-  long long t_loop = 0;  // thread 0: the serial decision loop alone
   int64_t nblocks = 0;
   int ins_hist[4] = {0, 0, 0, 0};  // thread 0: insertions of the last four blocks
   while (*flag) {
@@ -394,74 +401,55 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     pro_cand += ncand;
     __syncthreads();
     const long long tc = clock64();
-    // 3d. thread 0 applies search.py:148-154 in order (float64 compares):
-    //     refine iff fast < bound + sigma, insert iff exact < T (heapreplace:
-    //     the root is replaced and sifted down; bound = fast of the new root)
-    if (tid == 0) {
+    // 3d. warp 0 applies search.py:148-154 in order (float64 compares), 32
+    //     candidates per window: refine iff fast < bound + sigma, insert iff
+    //     exact < T.  The first inserting lane ends the window's decided
+    //     prefix (the bound moves there); the lanes after it are re-tested
+    //     against the new bound.  The heap is the sorted-array WarpHeap.
+    if (warp == 0) {
       const int64_t ins_before = insertions;
-      const long long tl0 = clock64();
       const int64_t ins_limit = *pub_J >= kInfBudget ? INT64_MAX : insertions + *pub_J;
-      *cut = -1;
-      double T = he[0];
-      double thr = __dadd_rn(hf[0], p.sigma);
-      constexpr int G8 = 8;
-      for (int c0 = 0; c0 < ncand; c0 += G8) {
-        double fg[G8], eg[G8];
-        int32_t ig[G8];
-#pragma unroll
-        for (int u = 0; u < G8; ++u) {  // all shared-memory loads of the group first
-          const bool ok = c0 + u < ncand;
-          fg[u] = ok ? cf[c0 + u] : 0.0;
-          eg[u] = ok ? ce[c0 + u] : 0.0;
-          ig[u] = ok ? cid[c0 + u] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < G8; ++u) {
-          if (c0 + u >= ncand || !(fg[u] < thr)) continue;
-          const double e = eg[u];
-          const int32_t id = ig[u];
-          ++refinements;
-          record_survivor(c.surv, id);
-          if (!(e < T)) continue;
-          // 4-ary max-heap: replace the root, sift down (children 4i+1..4i+4)
-          int i = 0;
-          for (;;) {
-            const int c1 = 4 * i + 1;
-            if (c1 >= k) break;
-            double be = he[c1];
-            int32_t bi = hi[c1];
-            int cm = c1;
-#pragma unroll
-            for (int d = 1; d < 4; ++d) {
-              const int cd = c1 + d;
-              if (cd < k) {
-                const double ed = he[cd];
-                const int32_t id2 = hi[cd];
-                if (key_gt(ed, id2, be, bi)) { be = ed; bi = id2; cm = cd; }
-              }
-            }
-            if (!key_gt(be, bi, e, id)) break;
-            he[i] = be;
-            hf[i] = hf[cm];
-            hi[i] = bi;
-            i = cm;
-          }
-          he[i] = e;
-          hf[i] = fg[u];
-          hi[i] = id;
-          T = he[0];
-          thr = __dadd_rn(hf[0], p.sigma);
+      long long cut_id = -1;
+      double T = H.top_e();
+      double thr = __dadd_rn(H.top_f(), p.sigma);
+      for (int c0 = 0; c0 < ncand && cut_id < 0; c0 += 32) {
+        const int ci = c0 + lane;
+        const bool ok = ci < ncand;
+        const double fv = ok ? cf[ci] : 0.0;
+        const double ev = ok ? ce[ci] : 0.0;
+        const int32_t id = ok ? cid[ci] : 0;
+        uint32_t pending = __ballot_sync(kFull, ok);
+        while (pending) {
+          const bool mine = (pending >> lane) & 1u;
+          const bool ref = mine && fv < thr;
+          const bool ins = ref && ev < T;
+          const uint32_t im = __ballot_sync(kFull, ins);
+          const int first = im ? __ffs(im) - 1 : 31;
+          const uint32_t decided = pending & (first == 31 ? kFull : ((2u << first) - 1u));
+          const uint32_t rm = __ballot_sync(kFull, ref) & decided;
+          refinements += __popc(rm);
+          if ((rm >> lane) & 1u) record_survivor(c.surv, id);
+          pending &= ~decided;
+          if (!im) break;
+          const double ne = __shfl_sync(kFull, ev, first);
+          const double nf = __shfl_sync(kFull, fv, first);
+          const int32_t nid = __shfl_sync(kFull, id, first);
+          H.replace_max(ne, nid, nf, lane);
+          T = H.top_e();
+          thr = __dadd_rn(H.top_f(), p.sigma);
           ++insertions;
           if (insertions > ins_limit) {  // the prefilter threshold is spent: re-filter the rest
-            *cut = (long long)id + 1;
+            cut_id = (long long)nid + 1;
             break;
           }
         }
-        if (*cut >= 0) break;
       }
-      t_loop += clock64() - tl0;
-      ins_hist[nblocks & 3] = (int)(insertions - ins_before);
-      *ins_recent = ins_hist[0] + ins_hist[1] + ins_hist[2] + ins_hist[3];
+      H.store(lane);  // smem copy for the threshold below and the hand-off
+      if (lane == 0) {
+        *cut = cut_id;
+        ins_hist[nblocks & 3] = (int)(insertions - ins_before);
+        *ins_recent = ins_hist[0] + ins_hist[1] + ins_hist[2] + ins_hist[3];
+      }
     }
     __syncwarp();
     if (warp == 0) {
@@ -600,7 +588,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     st.pro_t[0] = tp[0];
     st.pro_t[1] = tp[1];
     st.pro_t[2] = tp[2];
-    st.pro_t[3] = t_loop;  // (was: blocks)
+    st.pro_t[3] = nblocks;
     st.hi = fhi;
     st.lo = flo;
     st.thr = thr;
@@ -610,6 +598,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     st.wide = wide ? 1 : 0;
     st.ovf_pages = 0;
     st.ovf_pool = 0;
+    st.skipped = 0;
     st.J = J;
     st.ins0 = insertions;
     st.done = 0;
@@ -753,6 +742,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     uint4 a[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) a[v] = ldg_stream(cptr + v * 32);
+#pragma unroll 2
     for (int it = 0; it < ntile; ++it, t += TILE) {
       uint4 x[V];
 #pragma unroll
@@ -896,7 +886,11 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           }
         }
       }
-      if (!overflow) {
+      if (overflow) {  // the replay rescans this slice: stop streaming it
+        if (lane == 0) atomicAdd((unsigned long long*)&p.qs[q].skipped,
+                                 (unsigned long long)max((int64_t)0, w_hi - (t + TILE)));
+        break;
+      } else {
         int gg = cnt + excl;
         // ids fit 32 bits (n < 2^31); chunk v of this lane starts at idb + v*IPC
         const uint32_t idb = (uint32_t)t + (uint32_t)(lane * N);
@@ -1397,7 +1391,7 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
       s[12] = (p.debug & 4) ? t_work : st.pro_t[0];  // debug bit 2: replay warp-0 timers
       s[13] = (p.debug & 4) ? t_wait : st.pro_t[1];
       s[14] = st.pro_t[2];
-      s[15] = st.pro_t[3];
+      s[15] = p.qs[q].skipped;
     }
   }
 }

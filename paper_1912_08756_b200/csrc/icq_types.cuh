@@ -37,6 +37,8 @@ struct QState {
   int64_t ins0;         // insertions when thr was set
   int32_t done;         // all items decided, outputs written
   int32_t rounds;       // filter/replay rounds used
+  int64_t skipped;      // items the filter did not stream (their slice overflowed:
+                        // the replay rescans it from the codes)
 };
 constexpr int32_t kInfBudget = 1 << 30;
 constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)

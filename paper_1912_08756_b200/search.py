@@ -34,7 +34,7 @@ STATS_NAMES = ("insertions", "replay_candidates", "filter_rounds", "prologue_end
                "prologue_cycles", "replay_cycles", "rescanned_slices", "wide",
                "prologue_f64_scored", "filter_candidates", "prologue_insertions",
                "filter_hi_f32_bits", "prologue_filter_cycles", "prologue_score_cycles",
-               "prologue_decide_cycles", "prologue_serial_loop_cycles")
+               "prologue_decide_cycles", "filter_skipped_items")
 
 
 @dataclass
