@@ -84,6 +84,18 @@ def main():
                 tot[name] = tot.get(name, 0.0) + float(r[vi])
             f.write("# share of device time: " + ", ".join(
                 f"{k} {100 * v / sum(tot.values()):.1f}%" for k, v in tot.items()) + "\n")
+            # the search step's own kernels: the pipeline instantiation launched
+            # most often (bench.py's setup also runs the exact engine once, <16>)
+            cnt = {}
+            for r in rows[1:]:
+                name = r[ki].split("(")[0].replace("void ", "")
+                if "icq_filter_kernel" in name:
+                    cnt[name] = cnt.get(name, 0) + 1
+            if cnt:
+                targ = max(cnt, key=cnt.get).split("icq_filter_kernel")[1]
+                step = {k: v for k, v in tot.items() if k.endswith(targ) or "lut_build" in k}
+                f.write(f"# share of the search step ({targ} pipeline + LUT build): " + ", ".join(
+                    f"{k} {100 * v / sum(step.values()):.1f}%" for k, v in step.items()) + "\n")
     traffic = {}
     tpath = PROF / "traffic.json"
     if tpath.exists():
