@@ -360,6 +360,7 @@ def main():
         "scan_ms_per_step": t_scan / args.steps * 1e3,
         "pruning": {"refined_fraction": float(refine.mean().item() / w.n),
                     "insertions_per_query": float(stats[:, 0].mean().item()),
+                    "prologue_insertions_per_query": float(stats[:, 10].mean().item()),
                     "replay_live_candidates_per_query": float(stats[:, 1].mean().item()),
                     "filter_rounds_per_query": float(stats[:, 2].mean().item()),
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),

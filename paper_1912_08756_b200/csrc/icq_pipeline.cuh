@@ -1038,7 +1038,7 @@ constexpr int kRP = (kRW - 1) * 32;  // preparing threads
 constexpr int kMaxChunks = 512;   // chunk descriptors per slice group
 
 template <int FP>
-__global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_constant__ PipeParams p) {
+__global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_constant__ PipeParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
@@ -1214,10 +1214,25 @@ __global__ void __launch_bounds__(kRW * 32) icq_replay_kernel(const __grid_const
           if (f < thr && !(p.debug & 2)) plist[atomicAdd((int*)&ctl[2], 1)] = i;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
-        const int nl = ctl[2];
-        for (int jj = ptid; jj < nl; jj += kRP) {
-          const int idx = plist[jj];
-          ex[idx] = exact64(lut, m, K, false, load_row(p.codes_full, p.KP, (int32_t)src[idx].x));
+        // exact scores of the entries under the published bound (debug bit 3:
+        // of every entry -- measured slower: the extra row reads outweigh
+        // warp 0's serial reads when the live bound rises past the published
+        // one).  Rows are read in batches of kXB per thread so their
+        // latencies overlap.
+        const int nl = (p.debug & 8) ? len : ctl[2];
+        constexpr int kXB = 6;
+        for (int j0 = ptid; j0 < nl; j0 += kXB * kRP) {
+          Row rows[kXB];
+          int idx[kXB];
+#pragma unroll
+          for (int r = 0; r < kXB; ++r) {
+            const int jj = j0 + r * kRP;
+            idx[r] = jj < nl ? ((p.debug & 8) ? jj : (int)plist[jj]) : -1;
+            if (idx[r] >= 0) rows[r] = load_row(p.codes_full, p.KP, (int32_t)src[idx[r]].x);
+          }
+#pragma unroll
+          for (int r = 0; r < kXB; ++r)
+            if (idx[r] >= 0) ex[idx[r]] = exact64(lut, m, K, false, rows[r]);
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
         if (ptid == 0) ctl[2] = 0;
