@@ -28,7 +28,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -62,63 +61,78 @@ def _profiled_traffic(cfg: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and clock-event (throttle) reasons during the timed region,
+    sampled in-process through NVML every 20 ms.  (An `nvidia-smi -lms 20`
+    child, the first version, stalled the launch path for 5-70 ms in about
+    half of the c4 runs; NVML clock queries measured clean.)"""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+             ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm MHz, max sm MHz, reason bits)
         self._stop = threading.Event()
-        self._proc = None
+        self._t = None
         self.recording = False  # rows are kept only while the timed region runs
         self._first = threading.Event()
+        self._nv = None
+        self._h = None
+
+    def _handle(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        self._nv = nv
+        try:  # the NVML device of this CUDA device (CUDA_VISIBLE_DEVICES may remap)
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        if os.environ.get("ICQ_BENCH_NO_CLOCKS"):  # (diagnostics: timing without the sampler)
+            return self
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except OSError:
-            self._proc = None
+            self._h = self._handle()
+            self._mx = self._nv.nvmlDeviceGetMaxClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+        except Exception:
+            self._h = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rb = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                break
             self._first.set()
             if self.recording:
-                self.rows.append([x.strip() for x in line.split(",")])
+                self.rows.append((float(sm), float(self._mx), int(rb)))
+            self._stop.wait(0.02)
 
     def wait_started(self, timeout=10.0):
-        """nvidia-smi is started before the warm-up (its start-up stalls the
-        driver); wait for its first sample so that happens outside timing."""
-        if self._proc is not None:
+        if self._t is not None:
             self._first.wait(timeout)
 
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        reasons = sorted({nm for r in self.rows for nm, bit in self.NAMES if r[2] & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
+                "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "NVML, 20 ms"}
 
 
 # ---------------------------------------------------------------------------
