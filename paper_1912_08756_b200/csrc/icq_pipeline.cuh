@@ -691,13 +691,14 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     if (q != cur_q) {
       __syncthreads();  // every warp is done with the previous query's pages
       const double* glut = p.lut64 + (size_t)q * K * m;
-      for (int i = tid; i < FP * m * G::R; i += kFW * 32) {
-        const int s = i / (m * G::R);
-        const int rem = i - s * (m * G::R);
-        const int j = rem / G::R;
-        const int rr = rem - j * G::R;
+      // one table entry per thread and pass (a single L2 read), written to
+      // its R lane replicas with 16-byte stores
+      for (int i = tid; i < FP * m; i += kFW * 32) {
+        const int s = i / m, j = i - s * m;
         const float v = s < F ? __double2float_rn(glut[p.fast_books[s] * m + j]) : 0.f;
-        sts_f32(kPage * (1 + s / G::BPR) + j * 256 + (s % G::BPR) * 4 * G::R + rr * 4, v);
+        const uint32_t a0 = kPage * (1 + s / G::BPR) + j * 256 + (s % G::BPR) * 4 * G::R;
+#pragma unroll
+        for (int rr = 0; rr < G::R; rr += 4) sts_f32x4(a0 + rr * 4, v);
       }
       for (int i = tid; i < F * m; i += kFW * 32) {  // float64 fast tables (near-ties)
         const int s = i / m, j = i - s * m;

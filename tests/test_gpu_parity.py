@@ -85,6 +85,10 @@ CONFIGS = [
 #   subbatch  - as filter, queries in sub-batches of 4
 #   rounds    - as filter, insertion budget 1: several filter/replay rounds
 #   rounds3   - budget 0 and 3 rounds: the last round filters with M
+#   noprep    - as filter, the replay's preparing warps score nothing exactly:
+#               warp 0 reads every refined row itself (ICQ_DEBUG bit 1)
+#   allexact  - as filter, the preparing warps score every entry (bit 3)
+#   noties    - as filter, no tuple-tie rejection in the filter (bit 0)
 MODES = {
     "default": {},
     "filter": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"},
@@ -94,6 +98,9 @@ MODES = {
     # round re-filters the rest (the third round filters with M, unbudgeted)
     "rounds": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "1", "ICQ_ROUNDS": "8"},
     "rounds3": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "0", "ICQ_ROUNDS": "3"},
+    "noprep": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "2"},
+    "allexact": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "8"},
+    "noties": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "1"},
 }
 
 
