@@ -386,13 +386,20 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   }
   p.pro_min = env_i("ICQ_PRO_MIN", 8192);
   {
-    int64_t pm = h->n / 16;
-    if (pm < ((int64_t)1 << 18)) pm = (int64_t)1 << 18;
+    // prologue length cap: queries whose stale threshold stays loose are
+    // better handed to the filter early (measured: c1/c2/c4 best at 64k items,
+    // c5 (100M) at ~256k; the stop rule ends most queries well before)
+    int64_t pm = h->n / 384;
+    if (pm < ((int64_t)1 << 16)) pm = (int64_t)1 << 16;
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
   }
   {
-    int64_t entries = (int64_t)Qb * h->n / 32;
-    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)256 << 20;
+    // candidate pool: a shared bump allocator of 128-entry pages; when it runs
+    // dry every slice still growing overflows into a full exact rescan (c2
+    // at n/32: ~57 of 64 slices per query), so it is sized generously --
+    // HBM is plentiful, the pool is never cleared (only its top counter)
+    int64_t entries = (int64_t)Qb * h->n / 8;
+    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 30;  // <= 16 GiB
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
     p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
   }
