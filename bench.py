@@ -117,6 +117,18 @@ class ClockSampler:
                 self.rows.append((float(sm), float(self._mx), int(rb)))
             self._stop.wait(0.02)
 
+    def sample_now(self):
+        """One sample from the calling thread (short timed regions: taken
+        while the enqueued steps still run)."""
+        if self._h is None:
+            return
+        try:
+            sm = self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM)
+            rb = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.rows.append((float(sm), float(self._mx), int(rb)))
+        except Exception:
+            pass
+
     def wait_started(self, timeout=10.0):
         if self._t is not None:
             self._first.wait(timeout)
@@ -261,6 +273,7 @@ def main():
     clk.recording = True
     for i in range(args.steps):
         outs.append(step(args.warmup + i, evs[i]))
+    clk.sample_now()  # the last steps are still running on the device
     torch.cuda.synchronize()
     clk.recording = False
     clk.__exit__(None, None, None)
