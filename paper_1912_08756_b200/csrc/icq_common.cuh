@@ -15,6 +15,7 @@
 namespace icq {
 
 #define kInf (__int_as_float(0x7f800000))
+#define kInf64 (__longlong_as_double(0x7ff0000000000000LL))
 
 // --------------------------------------------------------------------------
 // code rows and float64 scores in the reference's order (search.py:94)

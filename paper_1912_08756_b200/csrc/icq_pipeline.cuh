@@ -950,7 +950,8 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
                                               const uint2 (&tail)[kWU], const double (&ex)[kWU],
                                               const bool (&valid)[kWU], int32_t* sid,
                                               int32_t* sidx, double* sfv, double* sfe,
-                                              const double* lutf) {
+                                              const double* lutf, double cap = __builtin_huge_val(),
+                                              int* brk = nullptr) {
   int pos0 = 0;  // first undecided window position (u * 32 + lane)
   const uint32_t lt = (1u << lane) - 1u;
   for (;;) {
@@ -1015,6 +1016,11 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
           if (lane == 0) *c.stop_pos = (int64_t)nid + 1;
           __syncwarp();
           return true;
+        }
+        if (brk && L.thr64 > cap) {  // bound rose above the caller's pre-filter: it walks on
+          *brk = __shfl_sync(kFull, wpos, first);
+          __syncwarp();
+          return false;
         }
         if (L.thr64 > thr) {  // bound rose: re-compact everything after the insertion
           pos0 = __shfl_sync(kFull, wpos, first) + 1;
@@ -1256,46 +1262,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch+1 landed
           asm volatile("bar.sync 1, %0;" ::"n"(kRP));
           prep(ch + 1);
-        } else if (chunk[3 * ch + 2] >= 0) {
-          // candidates overflowed this slice's pages: rescan its items from the codes
-          const int64_t j = g0 + chunk[3 * ch + 2];
-          const int64_t lo = max(j * SW, st.P), hi_ = min((j + 1) * SW, n);
-          if (lo < hi_) ++fallback_slices;
-          for (int64_t i0 = lo; i0 < hi_; i0 += kWU * 32) {
-            int32_t ids2[kWU];
-            float f2[kWU];
-            uint2 t2[kWU];
-            double e2[kWU];
-            bool valid2[kWU];
-#pragma unroll
-            for (int u = 0; u < kWU; ++u) {
-              const int64_t i = i0 + u * 32 + lane;
-              valid2[u] = i < hi_;
-              ids2[u] = (int32_t)i;
-              f2[u] = -kInf;  // no float32 score: the exact float64 one decides
-              t2[u] = make_uint2(0u, 0u);
-              e2[u] = __longlong_as_double(0x7ff8000000000000LL);
-              if (valid2[u]) {
-                const Row r2 = load_fast_row(p.codes_fast, FP, i);
-                if constexpr (FP <= 8) {
-                  t2[u] = make_uint2(r2.w[0], r2.w[1]);
-                } else {
-                  double x = 0.0;  // float64 fast score in the reference's order
-#pragma unroll
-                  for (int s2 = 0; s2 < FP; ++s2)
-                    if (s2 < F) x = __dadd_rn(x, lutf[s2 * m + (int)r2.byte(s2)]);
-                  const unsigned long long db = (unsigned long long)__double_as_longlong(x);
-                  t2[u] = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
-                }
-              }
-            }
-            if (replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf)) {
-              if (lane == 0) ctl[3] = 1;
-              break;
-            }
-          }
-          if (lane == 0) *pub_thr = L.thr64;
-        } else {
+        } else if (chunk[3 * ch + 2] < 0) {
           const uint4* src = ring + (ch % kRSlots) * kCH;
           const double* exs = ring_e + (ch % kRSlots) * kCH;
           const int len = chunk[3 * ch + 1];
@@ -1321,6 +1288,135 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             }
           }
           if (lane == 0) *pub_thr = L.thr64;
+        }
+        if (chunk[3 * ch + 2] >= 0) {  // (CTA-uniform)
+          // candidates overflowed this slice's pages: rescan its items from the
+          // codes.  All four warps pre-filter a sub-range against T = the live
+          // bound + sigma (bit masks in this chunk's idle ring slot); warp 0
+          // decides the flagged items in order.  Unflagged items have fast >=
+          // T, so they stay unrefined until an insertion lifts the bound above
+          // T: the next sub-range then starts right after that insertion,
+          // pre-filtered against the new bound.
+          __syncthreads();
+          const int64_t j = g0 + chunk[3 * ch + 2];
+          const int64_t lo = max(j * SW, st.P), hi_ = min((j + 1) * SW, n);
+          if (lo < hi_ && tid == 0) ++fallback_slices;
+          uint32_t* rmask = reinterpret_cast<uint32_t*>(ring + (ch % kRSlots) * kCH);  // 8 KiB
+          int32_t* rlst = reinterpret_cast<int32_t*>(ring_e + (ch % kRSlots) * kCH);  // 4 KiB
+          volatile double* tsub = reinterpret_cast<volatile double*>(ctl + 8);
+          constexpr int kSub = kCH * 16 * 8;  // items per sub-range: 2048 mask words (8 KiB)
+          auto fast_at = [&](int64_t i, uint2& tup) -> double {
+            const Row r2 = load_fast_row(p.codes_fast, FP, i);
+            double x;
+            if constexpr (FP <= 8) {
+              tup = make_uint2(r2.w[0], r2.w[1]);
+              x = tuple_f64<FP>(tup, lutf, m, F);
+            } else {
+              x = 0.0;  // float64 fast score in the reference's order
+#pragma unroll
+              for (int s2 = 0; s2 < FP; ++s2)
+                if (s2 < F) x = __dadd_rn(x, lutf[s2 * m + (int)r2.byte(s2)]);
+              const unsigned long long db = (unsigned long long)__double_as_longlong(x);
+              tup = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+            }
+            return x;
+          };
+          // one decision window over items given by position -> id
+          auto walk = [&](auto id_at, int npos, int p0, double cap, int* brk) -> bool {
+            for (int w0 = p0; w0 < npos; w0 += kWU * 32) {
+              int32_t ids2[kWU];
+              float f2[kWU];
+              uint2 t2[kWU];
+              double e2[kWU];
+              bool valid2[kWU];
+#pragma unroll
+              for (int u = 0; u < kWU; ++u) {
+                const int x = w0 + u * 32 + lane;
+                valid2[u] = x < npos;
+                const int64_t i = valid2[u] ? id_at(x) : 0;
+                ids2[u] = (int32_t)i;
+                f2[u] = -kInf;  // no float32 score: the exact float64 one decides
+                t2[u] = make_uint2(0u, 0u);
+                e2[u] = __longlong_as_double(0x7ff8000000000000LL);
+                if (valid2[u]) (void)fast_at(i, t2[u]);
+              }
+              int b = -1;
+              if (replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf,
+                                    cap, brk ? &b : nullptr))
+                return true;
+              if (b >= 0) { *brk = w0 + b; return false; }
+            }
+            return false;
+          };
+          bool stopped = false;
+          volatile long long* snext = reinterpret_cast<volatile long long*>(ctl + 10);
+          for (int64_t s0 = lo; s0 < hi_ && !stopped;) {
+            const int64_t s1 = min(hi_, s0 + (int64_t)kSub);
+            const int nsub = (int)(s1 - s0);
+            if (warp == 0 && lane == 0) *tsub = (p.debug & 16) ? -kInf64 : L.thr64;
+            __syncthreads();
+            const double T = *tsub;
+            // kWU words per warp and pass: the row reads of a pass overlap
+            for (int b0 = warp * 32 * kWU; b0 < nsub; b0 += kRW * 32 * kWU) {
+              Row rows[kWU];
+#pragma unroll
+              for (int u = 0; u < kWU; ++u) {
+                const int x = b0 + u * 32 + lane;
+                if (x < nsub) rows[u] = load_fast_row(p.codes_fast, FP, s0 + x);
+              }
+#pragma unroll
+              for (int u = 0; u < kWU; ++u) {
+                const int x = b0 + u * 32 + lane;
+                bool under = false;
+                if (x < nsub) {
+                  double f = 0.0;  // float64 fast score in the reference's order
+#pragma unroll
+                  for (int s2 = 0; s2 < FP; ++s2)
+                    if (s2 < F) f = __dadd_rn(f, lutf[s2 * m + (int)rows[u].byte(s2)]);
+                  under = f < T;
+                }
+                const uint32_t bw = __ballot_sync(kFull, under);
+                if (lane == 0 && b0 + u * 32 < nsub) rmask[(b0 >> 5) + u] = bw;
+              }
+            }
+            __syncthreads();
+            if (warp == 0) {
+              int from = 0;  // sub-range position where the one-by-one walk starts
+              int64_t next = s1;
+              if (L.thr64 <= T) {
+                from = nsub;
+                const int nwords = (nsub + 31) >> 5;
+                for (int w0 = 0; w0 < nwords && !stopped; w0 += 32) {
+                  const uint32_t wv = w0 + lane < nwords ? rmask[w0 + lane] : 0u;
+                  const int cw = __popc(wv);
+                  int incl = cw;
+#pragma unroll
+                  for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                  }
+                  const int nl = __shfl_sync(kFull, incl, 31);
+                  int o = incl - cw;
+                  for (uint32_t bb = wv; bb; bb &= bb - 1) rlst[o++] = (w0 + lane) * 32 + __ffs(bb) - 1;
+                  __syncwarp();
+                  int brk = -1;
+                  stopped = walk([&](int x) { return s0 + rlst[x]; }, nl, 0, T, &brk);
+                  __syncwarp();
+                  if (brk >= 0) { next = s0 + rlst[brk] + 1; break; }  // bound rose above T
+                }
+              }
+              if (!stopped && from < nsub)
+                stopped = walk([&](int x) { return s0 + x; }, nsub, from, kInf64, nullptr);
+              if (lane == 0) {
+                if (stopped) ctl[3] = 1;
+                *snext = (long long)next;
+              }
+            }
+            __syncthreads();
+            stopped = ctl[3] != 0;
+            s0 = (int64_t)*snext;
+          }
+          if (warp == 0 && lane == 0) *pub_thr = L.thr64;
         }
         const long long tw1 = clock64();
         __syncthreads();

@@ -89,6 +89,7 @@ CONFIGS = [
 #               warp 0 reads every refined row itself (ICQ_DEBUG bit 1)
 #   allexact  - as filter, the preparing warps score every entry (bit 3)
 #   noties    - as filter, no tuple-tie rejection in the filter (bit 0)
+#   overflow_walk - as overflow, rescans walked item by item by warp 0 (bit 4)
 MODES = {
     "default": {},
     "filter": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"},
@@ -101,6 +102,9 @@ MODES = {
     "noprep": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "2"},
     "allexact": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "8"},
     "noties": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "1"},
+    # overflow rescans without the cooperative pre-filter (warp 0 walks all)
+    "overflow_walk": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_POOL_PAGES": "2",
+                      "ICQ_DEBUG": "16"},
 }
 
 
