@@ -1356,16 +1356,17 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             if (warp == 0 && lane == 0) *tsub = (p.debug & 16) ? -kInf64 : L.thr64;
             __syncthreads();
             const double T = *tsub;
-            // kWU words per warp and pass: the row reads of a pass overlap
-            for (int b0 = warp * 32 * kWU; b0 < nsub; b0 += kRW * 32 * kWU) {
-              Row rows[kWU];
+            constexpr int kPW = 16;
+            // kPW words per warp and pass: the row reads of a pass overlap
+            for (int b0 = warp * 32 * kPW; b0 < nsub; b0 += kRW * 32 * kPW) {
+              Row rows[kPW];
 #pragma unroll
-              for (int u = 0; u < kWU; ++u) {
+              for (int u = 0; u < kPW; ++u) {
                 const int x = b0 + u * 32 + lane;
                 if (x < nsub) rows[u] = load_fast_row(p.codes_fast, FP, s0 + x);
               }
 #pragma unroll
-              for (int u = 0; u < kWU; ++u) {
+              for (int u = 0; u < kPW; ++u) {
                 const int x = b0 + u * 32 + lane;
                 bool under = false;
                 if (x < nsub) {
