@@ -1350,7 +1350,16 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           };
           bool stopped = false;
           volatile long long* snext = reinterpret_cast<volatile long long*>(ctl + 10);
-          for (int64_t s0 = lo; s0 < hi_ && !stopped;) {
+          if constexpr (FP > 2) {
+            // wider fast codes (c3/c4 shapes) rarely overflow: warp 0 walks the
+            // slice alone and the kernel keeps its smaller register footprint
+            if (warp == 0) {
+              stopped = walk([&](int x) { return lo + x; }, (int)max((int64_t)0, hi_ - lo), 0,
+                             kInf64, nullptr);
+              if (lane == 0 && stopped) ctl[3] = 1;
+            }
+          }
+          for (int64_t s0 = lo; FP <= 2 && s0 < hi_ && !stopped;) {
             const int64_t s1 = min(hi_, s0 + (int64_t)kSub);
             const int nsub = (int)(s1 - s0);
             if (warp == 0 && lane == 0) *tsub = (p.debug & 16) ? -kInf64 : L.thr64;
