@@ -393,6 +393,9 @@ def main():
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),
                     "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
                     "replay_cycles_per_query": float(stats[:, 5].mean().item()),
+                    "replay_cycles_max_query": [float(stats[:, 5].max().item()), int(stats[:, 5].argmax().item()),
+                                                float(stats[stats[:, 5].argmax(), 9].item()),
+                                                float(stats[stats[:, 5].argmax(), 3].item())],
                     "rescanned_slices": int((stats[:, 6].long() & 0xFFFFF).sum().item()),
                     "overflow_slices_pages": int(((stats[:, 6].long() >> 20) & 0xFFFFF).sum().item()),
                     "overflow_slices_pool": int((stats[:, 6].long() >> 40).sum().item()),
