@@ -128,10 +128,11 @@ static __device__ void heap_replace_max(double* he, double* hf, int32_t* hi, int
 // 4l..4l+3): an insertion shifts registers locally, moves only the lane
 // boundary entry with one shuffle per field, and finds its position with one
 // __reduce_add_sync.  Larger k keeps the sorted array in shared memory.  A
-// warp-uniform copy of the top two entries gives the new maximum (T and
-// bound) after an insertion with plain per-lane ALU work.
+// warp-uniform copy of the top entry (refreshed by shuffles from lane 0 after
+// each insertion) gives T and the bound; a deeper uniform cache (2 or 4
+// entries, kept sorted with per-lane ALU work) measured slower.
 constexpr int kRegHeapRegs = 4;
-constexpr int kTopC = 2;
+constexpr int kTopC = 1;
 struct WarpHeap {
   int k;
   bool reg;
