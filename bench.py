@@ -3,8 +3,8 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl b200|reference]
 
-Workload: one BASELINE config (default c4 = the 10M-item scan-bound config the
-north-star roofline target names; c1..c5 selectable with --config),
+Workload: one BASELINE config (default c5 = configs[4], the largest
+single-GPU config: 100M items, batch 512; c1..c5 selectable with --config),
 seeded synthetic data (tools/workloads.py), books trained by the reference
 (bench_data/), database encoded on the GPU.  A step = one batch of queries
 through the hot path (K1 LUT build + fused scan/prune/refine/top-k kernel).
@@ -18,7 +18,10 @@ roofline effective code-stream bandwidth of the scan kernel:
          HBM copy peak (MEASURED_PEAKS.json)
 cpu_baseline the reference algorithm's CPU port (oracle.two_step_loop, a
          literal restatement of search.py:112-165) on a bounded query sample,
-         all host cores, rank 0 at N=1.
+         as many host processes as cores and RAM allow, rank 0 at N=1.
+sigma_sweep  the same batch pipeline at sigma in {mean lambda, 4 mean lambda,
+         learned}: q/s, refined fraction, list (filter pass) fraction, items
+         walked in order, recall@k against the exact engine.
 Multi-GPU: query batches are independent -> replicas, no collective
 (scaling "weak": each rank runs the same number of batches).
 """
@@ -162,6 +165,20 @@ def _cpu_one(qi):
     return qi, r.ids, r.scores, r.ops.refinements, time.perf_counter() - t0
 
 
+def cpu_workers(w, cap=None):
+    """Host processes for the CPU port: every core, bounded by RAM -- each
+    in-flight query materialises (n, K) gathers plus two Python lists of n
+    floats (search.py:94, :146-147), ~ n * (16 K + 80) bytes."""
+    import psutil
+
+    cores = os.cpu_count() or 1
+    per_q = w.n * (16 * w.K + 80)
+    avail = psutil.virtual_memory().available - (8 << 30)
+    by_ram = max(1, int(avail // per_q))
+    n = min(cores, by_ram)
+    return min(n, cap) if cap else n
+
+
 def cpu_baseline(books, codes_host, fast, sigma, Qhost, k, nq, workers):
     import multiprocessing as mp
 
@@ -179,7 +196,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c4"),
+    ap.add_argument("--config", default=os.environ.get("ICQ_BENCH_CONFIG", "c5"),
                     choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--sigma", type=float, default=None, help="override the learned margin")
@@ -187,6 +204,8 @@ def main():
     ap.add_argument("--cpu-queries", type=int, default=0, help="CPU baseline sample (0 = auto)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the sigma sweep")
+    ap.add_argument("--sweep-steps", type=int, default=3)
     args = ap.parse_args()
 
     import torch
@@ -352,20 +371,24 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         codes_h = codes.cpu().numpy()
-        nqc = args.cpu_queries or max(8, min(64, int(2.0e8 // max(1, w.n * w.K))))
-        workers = min(os.cpu_count() or 1, nqc)
-        if w.n >= 50_000_000:
-            workers = min(workers, 2)  # ~10-17 GB of temporaries per in-flight query
+        workers = cpu_workers(w)
+        # one query per process, at least 8 queries (two rounds on small hosts)
+        nqc = args.cpu_queries or (max(8, workers) if w.n < 50_000_000 else workers)
         Qh = Qall[:nqc].cpu().numpy()
-        res, wall = cpu_baseline(books, codes_h, fast, sigma, Qh, w.k, nqc, workers)
+        res, wall = cpu_baseline(books, codes_h, fast, sigma, Qh, w.k, nqc, min(workers, nqc))
         ids, sc, rf, _ = dev.search_host(Qh, w.k, sigma, exact=False)
         mism = sum(int(not (np.array_equal(ids[qi], r_ids) and np.array_equal(sc[qi], r_sc)
                             and rf[qi] == r_rf)) for qi, r_ids, r_sc, r_rf, _ in res)
-        cpu = {"value": nqc / wall, "unit": "queries/s", "cores": workers, "kind": "port",
+        cpu = {"value": nqc / wall, "unit": "queries/s", "cores": min(workers, nqc), "kind": "port",
                "sample": f"{nqc} queries of {w.name} (first {nqc} of the query set), oracle."
-                         f"two_step_loop (literal search.py:112-165), {workers} processes",
+                         f"two_step_loop (literal search.py:112-165), {min(workers, nqc)} processes",
                "cpu_seconds": sum(r[4] for r in res),
                "parity_vs_gpu": {"queries": nqc, "mismatches": mism}}
+        del codes_h
+
+    sweep = None
+    if not args.no_sweep:
+        sweep = sigma_sweep(args, w, dev, meta, sigma, batch, flush, stream, ex, Qall)
 
     line = {
         "metric": "queries/sec (top-k two-step ICQ search); G code-lookups/s; fast-scan GB/s vs roofline",
@@ -389,7 +412,9 @@ def main():
                     "insertions_per_query": float(stats[:, 0].mean().item()),
                     "prologue_insertions_per_query": float(stats[:, 10].mean().item()),
                     "replay_live_candidates_per_query": float(stats[:, 1].mean().item()),
-                    "filter_rounds_per_query": float(stats[:, 2].mean().item()),
+                    "walked_items_per_query": float(stats[:, 2].mean().item()),
+                    "walked_items_max_query": float(stats[:, 2].max().item()),
+                    "rounds_per_query": float((stats[:, 7].long() >> 8).double().mean().item()),
                     "prologue_items_per_query": float(stats[:, 3].mean().item()),
                     "prologue_cycles_per_query": float(stats[:, 4].mean().item()),
                     "replay_cycles_per_query": float(stats[:, 5].mean().item()),
@@ -399,7 +424,7 @@ def main():
                     "rescanned_slices": int((stats[:, 6].long() & 0xFFFFF).sum().item()),
                     "overflow_slices_pages": int(((stats[:, 6].long() >> 20) & 0xFFFFF).sum().item()),
                     "overflow_slices_pool": int((stats[:, 6].long() >> 40).sum().item()),
-                    "wide_queries": int(stats[:, 7].sum().item()),
+                    "wide_queries": int((stats[:, 7].long() & 0xFF).sum().item()),
                     "prologue_f64_scored_per_query": float(stats[:, 8].mean().item()),
                     "filter_candidates_per_query": float(stats[:, 9].mean().item()),
                     "filter_skipped_items_per_query": float(stats[:, 15].mean().item()),
@@ -407,8 +432,7 @@ def main():
                     "prologue_phase_cycles_per_query": {
                         "prefilter": float(stats[:, 12].mean().item()),
                         "score": float(stats[:, 13].mean().item()),
-                        "decide": float(stats[:, 14].mean().item()),
-                        "serial_loop": float(stats[:, 15].mean().item())},
+                        "decide": float(stats[:, 14].mean().item())},
                     "recall_vs_exact": recall},
         "roofline": {"bound": "hbm", "achieved": filter_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": filter_gbs / hbm_peak, "traffic": _profiled_traffic(w.name),
@@ -426,6 +450,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": 4 * args.steps,
         "cpu_baseline": cpu,
+        "sigma_sweep": sweep,
         "setup_seconds": prep_s,
     }
     if rank == 0:
@@ -435,13 +460,59 @@ def main():
     return 0
 
 
+def sigma_sweep(args, w, dev, meta, sigma0, batch, flush, stream, ex, Qall):
+    """The batch pipeline at the other operating points of SURVEY §8(d) rule
+    step 4: sigma in {mean lambda, 4 mean lambda} and the learned margin
+    (when it differs).  Device-timed like the headline (L2 flushed), one
+    JSON object per sigma; recall@k against the exact engine on batch 0."""
+    import torch
+
+    lam = float(np.asarray(meta["lambdas"], dtype=np.float64).mean())
+    learned = float(meta["learned_sigma"])
+    pts = [("mean_lambda", lam), ("4_mean_lambda", 4 * lam)]
+    if learned not in (0.0, sigma0, lam, 4 * lam):
+        pts.append(("learned", learned))
+    ei = ex["ids"].cpu().numpy()
+    out = []
+    for label, sg in pts:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.sweep_steps)]
+        res = []
+        for i in range(1 + args.sweep_steps):  # one warm-up
+            qb = batch(i)
+            flush.zero_()
+            if i:
+                evs[i - 1][0].record(stream)
+            lut = dev.build_lut_device(qb)
+            o = dev.search_lut_device(lut, w.k, sg, stats=True)
+            if i:
+                evs[i - 1][1].record(stream)
+                res.append((qb.shape[0], o))
+        torch.cuda.synchronize()
+        t = sum(a.elapsed_time(b) for a, b in evs) / 1e3
+        nq = sum(r[0] for r in res)
+        st = torch.cat([r[1]["stats"] for r in res]).double()
+        rf = torch.cat([r[1]["refinements"] for r in res]).double()
+        two = dev.search_device(batch(0), w.k, sg)
+        ti = two["ids"].cpu().numpy()
+        recall = float(np.mean([np.isin(ti[i], ei[i]).mean() for i in range(ti.shape[0])]))
+        out.append({"sigma": sg, "label": label, "queries_per_s": nq / t,
+                    "ms_per_step": t / args.sweep_steps * 1e3,
+                    "refined_fraction": float(rf.mean().item() / w.n),
+                    "list_fraction": float(st[:, 9].mean().item() / w.n),
+                    "walked_items_per_query": float(st[:, 2].mean().item()),
+                    "recall_at_k_vs_exact": recall, "steps": args.sweep_steps})
+    return out
+
+
 def run_reference(args, w, books, codes, fast, sigma, Qall, base_config):
-    """--impl reference: the reference algorithm's CPU port on host cores."""
+    """--impl reference: the reference algorithm's CPU port on host cores
+    (one query per process; as many processes as cores and RAM allow)."""
     codes_h = codes.cpu().numpy()
-    nq = args.cpu_queries or max(8, min(32, int(1.0e8 // max(1, w.n * w.K))))
-    workers = min(os.cpu_count() or 1, nq)
-    if w.n >= 50_000_000:
-        workers = min(workers, 2)
+    # (n >= 50M: <= 8 processes, ~15 s per step, so 25 steps fit the driver's limit)
+    workers = cpu_workers(w, cap=8 if w.n >= 50_000_000 else None)
+    nq = args.cpu_queries or workers
+    workers = min(workers, nq)
     Qh = Qall.cpu().numpy()
     rates = []
     for i in range(args.warmup + args.steps):

@@ -39,6 +39,12 @@ typedef enum {
 
 typedef struct icq_index_s* icq_index_t;
 
+/* Search flags (icq_search_with_lut / icq_search_host `flags`). */
+#define ICQ_FLAG_EXACT 1     /* run search_exact (search.py:97-109) instead of two-step */
+#define ICQ_FLAG_SIGMA_F32 2 /* sigma is a numpy float32 scalar: reproduce numpy 2's
+                                promotion of `bound + sigma` (search.py:149) -- float32
+                                once the heap maximum is an inserted entry */
+
 /* Message of the last failing call on this host thread ("" if none). */
 const char* icq_last_error(void);
 
@@ -82,6 +88,9 @@ icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int
  * build_lut (search.py:61-69): lut[q][b][j] = sum_d (c[b][j][d] - q[d])^2 in
  * float64, summed in numpy's pairwise order (bitwise equal to the reference).
  *   q   : dev float64 [Q*d]      lut : dev float64 [Q*K*m]
+ * A non-finite query value -> ICQ_ERR_VALIDATION (search.py:51-52).  Like
+ * every entry point below, the call synchronizes `stream` before returning
+ * so that device-side validation and error words reach the caller.
  * ------------------------------------------------------------------------- */
 icq_status icq_build_lut(icq_index_t h, const double* q_dev, int32_t Q, double* lut_dev,
                          void* stream);
@@ -101,14 +110,18 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
  *                  (instrumentation for parity tests; NULL to skip)
  *   stats_dev    : optional int64 [Q*16] diagnostics per query (see
  *                  paper_1912_08756_b200.search.STATS_NAMES): heap insertions,
- *                  items decided by the replay, filter rounds, prologue end,
+ *                  items decided by the replay, items walked in order, prologue end,
  *                  prologue / replay cycles, rescanned slices (| overflow
  *                  counts << 20 / << 40), wide flag, prologue float64 scorings,
  *                  filter candidates, prologue insertions, filter threshold
  *                  (float32 bits), prologue phase cycles
  *   fallback_out : optional host int32; set to 1 when the fast set is empty and
  *                  the exact engine ran instead (search.py:127-131)
- * The call is asynchronous on `stream` (no host synchronisation).
+ * Kernels run on `stream`; the call synchronizes it once at the end and
+ * returns the call's device error word (non-finite query ->
+ * ICQ_ERR_VALIDATION, internal check failures -> ICQ_ERR_CUDA).  Concurrent
+ * calls on different streams are safe (all scratch is per call).
+ * sigma is used as a float64 value; see icq_search_with_lut for float32.
  * ------------------------------------------------------------------------- */
 icq_status icq_search_two_step(icq_index_t h, const double* q_dev, int32_t Q, int32_t k,
                                double sigma, int64_t* ids_dev, double* scores_dev,
@@ -122,20 +135,23 @@ icq_status icq_search_exact(icq_index_t h, const double* q_dev, int32_t Q, int32
                             void* workspace_dev, size_t workspace_bytes, void* stream);
 
 /* Same two engines on a precomputed float64 LUT (icq_build_lut output,
- * dev float64 [Q*K*m]); no workspace.  exact = 1 runs search_exact.  Lets a
+ * dev float64 [Q*K*m]); no workspace.  flags: ICQ_FLAG_EXACT runs search_exact,
+ * ICQ_FLAG_SIGMA_F32 reproduces the reference's arithmetic for a numpy
+ * float32 sigma (which must then be exactly a float32 value).  Lets a
  * caller reuse tables across calls and time the scan kernel on its own. */
 icq_status icq_search_with_lut(icq_index_t h, const double* lut_dev, int32_t Q, int32_t k,
-                               double sigma, int32_t exact, int64_t* ids_dev, double* scores_dev,
+                               double sigma, int32_t flags, int64_t* ids_dev, double* scores_dev,
                                int64_t* refine_dev, uint32_t* survivors_dev, int64_t* stats_dev,
                                int32_t* fallback_out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Host-buffer entry points (end-to-end: H2D of queries, search, D2H of results,
  * synchronous).  Same semantics as above; all pointers are host pointers.
- * `exact` = 0 -> two-step, 1 -> exact engine.
+ * flags as icq_search_with_lut (0 = two-step with a float64 sigma).
+ * Non-finite query values are rejected on the host before any device work.
  * ------------------------------------------------------------------------- */
 icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32_t k,
-                           double sigma, int32_t exact, int64_t* ids_host,
+                           double sigma, int32_t flags, int64_t* ids_host,
                            double* scores_host, int64_t* refine_host, int32_t* fallback_out);
 
 /* ---------------------------------------------------------------------------

@@ -163,6 +163,22 @@ def exact(books: np.ndarray, codes: np.ndarray, q, k: int) -> OracleResult:
     return OracleResult(ids=order.astype(np.int64), scores=scores[order], ops=ops)
 
 
+def _refine_mask(fs, bound, max_id, sigma, k):
+    """``fs < bound + sigma`` with the reference's scalar types (search.py:149).
+
+    The reference's heap caches np.float64 fast scores for the seeds
+    (search.py:141, ``fast_all[i]``) and Python floats for inserted entries
+    (:153, ``fast_list[i]``).  With a numpy float32 sigma, numpy 2 (NEP 50)
+    computes ``bound + sigma`` in float32 when bound is a Python float and then
+    compares ``fast_list[i] < float32`` in float32 too; with an np.float64
+    bound everything stays float64.
+    """
+    if isinstance(sigma, np.float32) and max_id >= k:
+        thr32 = np.float32(bound) + sigma
+        return fs.astype(np.float32) < thr32
+    return fs < bound + float(sigma)
+
+
 def two_step(books, codes, fast, sigma, q, k: int, chunk: int = 4096) -> OracleResult:
     """search_two_step, search.py:112-165, instrumented with the survivor list.
 
@@ -198,8 +214,7 @@ def two_step(books, codes, fast, sigma, q, k: int, chunk: int = 4096) -> OracleR
         es = exact_all[pos:end]
         while pos < end:
             off = pos - (end - len(fs))
-            thr = bound + sigma
-            refined = fs[off:] < thr
+            refined = _refine_mask(fs[off:], bound, -heap[0][1], sigma, k)
             ins = refined & (es[off:] < -heap[0][0])
             hit = np.flatnonzero(ins)
             stop = off + (int(hit[0]) + 1 if hit.size else len(fs) - off)
@@ -237,10 +252,13 @@ def two_step_loop(books, codes, fast, sigma, q, k: int) -> OracleResult:
         res.fallback = True
         return res
     table = lut(books, q)
-    fl = gather(table, codes, fast).tolist()
-    el = gather(table, codes, np.arange(K)).tolist()
-    heap = [(-el[i], -i, fl[i]) for i in range(k)]
+    fast_all = gather(table, codes, fast)
+    exact_all = gather(table, codes, np.arange(K))
+    # seeds cache numpy scalars, inserted entries Python floats (search.py:141, :153)
+    heap = [(-exact_all[i], -i, fast_all[i]) for i in range(k)]
     heapq.heapify(heap)
+    fl = fast_all.tolist()
+    el = exact_all.tolist()
     bound = heap[0][2]
     survivors = []
     for i in range(k, n):

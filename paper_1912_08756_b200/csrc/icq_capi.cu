@@ -4,6 +4,7 @@
 // (build_lut :61, search_exact :97, search_two_step :112) and the argument
 // layout of icq.data.SearchIndex (data.py:193-263).  Validation mirrors
 // search.py:47-58, :123-131 and data.py:145-176.
+#include <cmath>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -25,7 +26,6 @@ static thread_local std::string g_err;
 static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<cudaEvent_t> g_prof_events;  // groups of kProfEvents per batch
-static constexpr int kProfEvents = 2 + 2 * icq::kRounds;
 
 static icq_status fail(icq_status code, const char* fmt, ...) {
   char buf[512];
@@ -214,7 +214,7 @@ icq_status icq_profile_enable(int32_t on) {
 
 icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   std::lock_guard<std::mutex> g(g_prof_mu);
-  double acc[3] = {0, 0, 0};  // prologue, filter (all rounds), replay (all rounds)
+  double acc[3] = {0, 0, 0};  // prologue, filter, replay
   const int groups = (int)(g_prof_events.size() / kProfEvents);
   for (int i = 0; i < groups; ++i) {
     cudaEvent_t* e = &g_prof_events[kProfEvents * i];
@@ -233,7 +233,7 @@ icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   return ICQ_OK;
 }
 
-int32_t icq_abi_version(void) { return 1; }
+int32_t icq_abi_version(void) { return 2; }
 
 icq_status icq_index_create(const float* books, int32_t K, int32_t m, int32_t d,
                             const uint32_t* codes, int64_t n, const uint32_t* fast, int32_t F,
@@ -278,12 +278,39 @@ icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int
   return ICQ_OK;
 }
 
+// Device error word of one call: bit 0 filter shared-memory layout, bit 2
+// replay chunk descriptors dropped, bit 3 a query holds non-finite values.
+static icq_status check_call_errors(int32_t err) {
+  if (err & 8) return fail(ICQ_ERR_VALIDATION, "query contains non-finite values");
+  if (err & 1) return fail(ICQ_ERR_CUDA, "filter kernel shared-memory layout check failed");
+  if (err & 4) return fail(ICQ_ERR_CUDA, "replay dropped candidate chunks");
+  if (err) return fail(ICQ_ERR_CUDA, "device error word 0x%x", err);
+  return ICQ_OK;
+}
+
+// one int32 of pinned host memory per thread: the error word's landing slot
+static int32_t* host_err_slot() {
+  static thread_local int32_t* slot = nullptr;
+  if (!slot && cudaMallocHost((void**)&slot, sizeof(int32_t)) != cudaSuccess) slot = nullptr;
+  return slot;
+}
+
 icq_status icq_build_lut(icq_index_t h, const double* q, int32_t Q, double* lut, void* stream) {
   if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
   if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
   if (Q == 0) return ICQ_OK;
-  CUDA_TRY(launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, (cudaStream_t)stream));
-  return ICQ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* err = nullptr;
+  int32_t* herr = host_err_slot();
+  if (!herr) return fail(ICQ_ERR_NOMEM, "pinned error slot allocation failed");
+  CUDA_TRY(cudaMallocAsync((void**)&err, sizeof(int32_t), s));
+  cudaError_t e = cudaMemsetAsync(err, 0, sizeof(int32_t), s);
+  if (e == cudaSuccess) e = launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, err, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(err, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(ICQ_ERR_CUDA, "build_lut: %s", cudaGetErrorString(e));
+  return check_call_errors(*herr);
 }
 
 icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes) {
@@ -294,27 +321,29 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
 }
 
 static icq_status search_impl(icq_index_t h, const double* q, const double* lut_in, int32_t Q,
-                              int32_t k, double sigma, bool exact, int64_t* ids, double* scores,
+                              int32_t k, double sigma, int32_t flags, int64_t* ids, double* scores,
                               int64_t* refine, uint32_t* survivors, int64_t* stats,
                               int32_t* fallback_out, void* ws, size_t ws_bytes, cudaStream_t s) {
   if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  bool exact = (flags & ICQ_FLAG_EXACT) != 0;
   if (!(k >= 1 && (int64_t)k <= h->n))
     return fail(ICQ_ERR_VALIDATION, "k=%d out of range [1, %lld]", k, (long long)h->n);
   if (!exact && !(sigma >= 0)) return fail(ICQ_ERR_VALIDATION, "sigma must be >= 0, got %g", sigma);
+  if (!exact && (flags & ICQ_FLAG_SIGMA_F32) && (double)(float)sigma != sigma)
+    return fail(ICQ_ERR_VALIDATION, "ICQ_FLAG_SIGMA_F32 with a sigma that is not a float32 value");
   if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
   const bool fallback = !exact && h->F == 0;  // search.py:127-131
   if (fallback_out) *fallback_out = fallback ? 1 : 0;
   if (fallback) exact = true;
   if (Q == 0) return ICQ_OK;
+  int32_t* herr = host_err_slot();
+  if (!herr) return fail(ICQ_ERR_NOMEM, "pinned error slot allocation failed");
   const double* lut = lut_in;
   if (!lut) {
     size_t need = 0;
     icq_workspace_size(h, Q, k, &need);
     if (!ws || ws_bytes < need)
       return fail(ICQ_ERR_NOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, need);
-    double* w = reinterpret_cast<double*>(ws);
-    CUDA_TRY(launch_lut(h->books, q, w, h->K, h->m, h->d, Q, h->prog_dev, s));
-    lut = w;
   }
   if (survivors) {
     const int64_t words = (h->n + 31) / 32;
@@ -323,7 +352,6 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   PipeParams p;
   memset(&p, 0, sizeof(p));
   p.codes_full = h->codes_full;
-  p.error = h->err_dev;
   p.n = h->n;
   p.words = (h->n + 31) / 32;
   p.K = h->K;
@@ -344,13 +372,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     FP = h->FP;
     memcpy(p.fast_books, h->fast_books, sizeof(p.fast_books));
     p.sigma = sigma;
+    p.sigma_f32 = (flags & ICQ_FLAG_SIGMA_F32) ? 1 : 0;
   }
   // ---- plan: sub-batches, ranges, unit order, candidate pool -------------
-  static const int sms = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   auto env_i = [](const char* name, int64_t dflt) {
     const char* v = getenv(name);
     return v ? (int64_t)atoll(v) : dflt;
@@ -358,7 +387,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   const int Qmax = (int)env_i("ICQ_QBATCH", 2048);
   const int Qb = Q < Qmax ? Q : Qmax;
   const bool big = (int64_t)h->n * FP > (int64_t)48 << 20;  // fast stream larger than ~L2/2
-  p.range_major = big ? 1 : 0;
+  p.range_major = (int32_t)env_i("ICQ_RANGE_MAJOR", big ? 1 : 0);
   {
     const int64_t units = 8LL * sms;
     int64_t nr = (units + Qb - 1) / Qb;
@@ -370,34 +399,40 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     if (cap < ((int64_t)1 << 18)) cap = (int64_t)1 << 18;
     if (big) cap = (int64_t)4 << 20;
     if (rs > cap) rs = cap;
+    rs = env_i("ICQ_RANGE_ITEMS", rs);
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
   }
   p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 512);
   p.debug = (int32_t)env_i("ICQ_DEBUG", 0);  // experiments only; results stay exact
-  p.j0 = (int32_t)env_i("ICQ_J0", -1);        // tests: force the first-round insertion budget
+  // list threshold theta = A_J + sigma: J = 0 is the live threshold at the
+  // prologue end (sigma == 0: anything looser lists millions of items on c5);
+  // with sigma > 0 the margin dominates the lists and a deeper J spares walks
+  p.list_j = (int32_t)env_i("ICQ_LIST_J", p.sigma == 0.0 ? 0 : 32);
+  p.pro_live = (int32_t)env_i("ICQ_PRO_LIVE", 0);
   {
-    // insertion-budgeted filter rounds (experimental; 1 = one round with M)
-    int64_t r = env_i("ICQ_ROUNDS", 1);
-    const char* sl = getenv("ICQ_BUDGET_SLACK");
-    p.budget_slack = sl ? atof(sl) : 0.05;
-    p.max_rounds = (int32_t)(r < 1 ? 1 : (r > kRounds ? kRounds : r));
+    const int64_t r = env_i("ICQ_ROUNDS", 3);
+    p.rounds = (int32_t)(r < 1 ? 1 : (r > kMaxRounds ? kMaxRounds : r));
+    // one replay CTA walks ~1 item per clock; a filter round lists a query's
+    // rest on every SM: hand walks longer than ~n/64 (>= 1M items) over
+    int64_t wc = h->n / 64;
+    p.walk_cap = env_i("ICQ_WALK_CAP", wc < ((int64_t)1 << 20) ? ((int64_t)1 << 20) : wc);
   }
   p.pro_min = env_i("ICQ_PRO_MIN", 8192);
   {
     // prologue length cap: queries whose stale threshold stays loose are
-    // better handed to the filter early (measured: c1/c2/c4 best at 64k items,
-    // c5 (100M) at ~256k; the stop rule ends most queries well before)
+    // better handed to the filter early (the stop rule ends most queries
+    // well before)
     int64_t pm = h->n / 384;
     if (pm < ((int64_t)1 << 16)) pm = (int64_t)1 << 16;
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
   }
   {
     // candidate pool: a shared bump allocator of 128-entry pages; when it runs
-    // dry every slice still growing overflows into a full exact rescan (c2
-    // at n/32: ~57 of 64 slices per query), so it is sized generously --
-    // HBM is plentiful, the pool is never cleared (only its top counter)
+    // dry every slice still growing overflows into a walk of its items, so it
+    // is sized generously -- HBM is plentiful, the pool is never cleared
+    // (only its top counter)
     int64_t entries = (int64_t)Qb * h->n / 8;
     const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 30;  // <= 16 GiB
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
@@ -415,10 +450,11 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     }
   });
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t b_lut = lut ? 0 : al((size_t)Q * h->K * h->m * sizeof(double));
   const size_t b_qs = al(sizeof(QState) * Qb);
   const size_t b_he = al((size_t)Qb * k * 8), b_hi = al((size_t)Qb * k * 4);
   const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint4));
-  const size_t b_top = 256;  // pool_top + active[kRounds]
+  const size_t b_top = 256;  // pool_top, error word
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
   const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl;
   char* sc = nullptr;
@@ -431,11 +467,19 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.heap_i = reinterpret_cast<int32_t*>(o); o += b_hi;
     p.pool = reinterpret_cast<uint4*>(o); o += b_pool;
     p.pool_top = reinterpret_cast<int32_t*>(o);
-    p.active = p.pool_top + 1;
+    p.error = p.pool_top + 1;
     o += b_top;
     p.slices = reinterpret_cast<int32_t*>(o);
   }
+  (void)b_lut;
   icq_status st = ICQ_OK;
+  cudaError_t e = cudaMemsetAsync(p.error, 0, sizeof(int32_t), s);
+  if (e == cudaSuccess && !lut) {  // K1: the float64 LUTs of every query into the workspace
+    double* w = reinterpret_cast<double*>(ws);
+    e = launch_lut(h->books, q, w, h->K, h->m, h->d, Q, h->prog_dev, p.error, s);
+    lut = w;
+  }
+  if (e != cudaSuccess) st = fail(ICQ_ERR_CUDA, "search setup: %s", cudaGetErrorString(e));
   for (int q0 = 0; q0 < Q && st == ICQ_OK; q0 += Qb) {
     const int nq = Q - q0 < Qb ? Q - q0 : Qb;
     PipeParams b = p;
@@ -446,7 +490,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     b.refinements = refine ? refine + q0 : nullptr;
     b.survivors = (!exact && survivors) ? survivors + (size_t)q0 * p.words : nullptr;
     b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
-    cudaError_t e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t) * (1 + kRounds), s);
+    e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
     int unsupported = 0;
     cudaEvent_t* ev = nullptr;
     cudaEvent_t evs[kProfEvents];
@@ -466,43 +510,53 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
       st = fail(ICQ_ERR_UNSUPPORTED, "k=%d does not fit the on-chip heap for K=%d, m=%d", k,
                 h->K, h->m);
   }
+  // every entry point reports the device error word of its own call
+  if (st == ICQ_OK) {
+    e = cudaMemcpyAsync(herr, p.error, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) st = fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e));
+  }
   cudaFreeAsync(sc, s);
-  return st;
+  if (st != ICQ_OK) return st;
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return check_call_errors(*herr);
 }
 
 icq_status icq_search_two_step(icq_index_t h, const double* q, int32_t Q, int32_t k, double sigma,
                                int64_t* ids, double* scores, int64_t* refine, uint32_t* survivors,
                                int64_t* stats, int32_t* fallback_out, void* ws, size_t ws_bytes,
                                void* stream) {
-  return search_impl(h, q, nullptr, Q, k, sigma, false, ids, scores, refine, survivors, stats,
+  return search_impl(h, q, nullptr, Q, k, sigma, 0, ids, scores, refine, survivors, stats,
                      fallback_out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 icq_status icq_search_exact(icq_index_t h, const double* q, int32_t Q, int32_t k, int64_t* ids,
                             double* scores, void* ws, size_t ws_bytes, void* stream) {
-  return search_impl(h, q, nullptr, Q, k, 0.0, true, ids, scores, nullptr, nullptr, nullptr,
-                     nullptr, ws, ws_bytes, (cudaStream_t)stream);
+  return search_impl(h, q, nullptr, Q, k, 0.0, ICQ_FLAG_EXACT, ids, scores, nullptr, nullptr,
+                     nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 icq_status icq_search_with_lut(icq_index_t h, const double* lut_dev, int32_t Q, int32_t k,
-                               double sigma, int32_t exact, int64_t* ids_dev, double* scores_dev,
+                               double sigma, int32_t flags, int64_t* ids_dev, double* scores_dev,
                                int64_t* refine_dev, uint32_t* survivors_dev, int64_t* stats_dev,
                                int32_t* fallback_out, void* stream) {
   if (!lut_dev) return fail(ICQ_ERR_VALIDATION, "lut_dev is NULL");
-  return search_impl(h, nullptr, lut_dev, Q, k, sigma, exact != 0, ids_dev, scores_dev, refine_dev,
+  return search_impl(h, nullptr, lut_dev, Q, k, sigma, flags, ids_dev, scores_dev, refine_dev,
                      survivors_dev, stats_dev, fallback_out, nullptr, 0, (cudaStream_t)stream);
 }
 
 icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32_t k,
-                           double sigma, int32_t exact, int64_t* ids_host, double* scores_host,
+                           double sigma, int32_t flags, int64_t* ids_host, double* scores_host,
                            int64_t* refine_host, int32_t* fallback_out) {
   if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
   if (Q < 0) return fail(ICQ_ERR_VALIDATION, "Q=%d < 0", Q);
+  const bool exact = (flags & ICQ_FLAG_EXACT) != 0;
   if (!(k >= 1 && (int64_t)k <= h->n))
     return fail(ICQ_ERR_VALIDATION, "k=%d out of range [1, %lld]", k, (long long)h->n);
   if (!exact && !(sigma >= 0)) return fail(ICQ_ERR_VALIDATION, "sigma must be >= 0, got %g", sigma);
   if (fallback_out) *fallback_out = (!exact && h->F == 0) ? 1 : 0;
   if (Q == 0) return ICQ_OK;
+  for (int64_t i = 0; i < (int64_t)Q * h->d; ++i)  // search.py:51-52, before any device work
+    if (!std::isfinite(q_host[i])) return fail(ICQ_ERR_VALIDATION, "query contains non-finite values");
   cudaStream_t s = cudaStreamPerThread;
   size_t ws_bytes = 0;
   icq_workspace_size(h, Q, k, &ws_bytes);
@@ -526,25 +580,18 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
   int64_t* idd = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(qd) + al(qb));
   double* scd = reinterpret_cast<double*>(reinterpret_cast<char*>(idd) + al(ib));
   int64_t* rfd = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scd) + al(sb));
-  icq_status st = ICQ_OK;
-  cudaError_t e = cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) {
-    st = search_impl(h, qd, nullptr, Q, k, sigma, exact != 0, idd, scd, rfd, nullptr, nullptr,
-                     nullptr, ws, ws_bytes, s);
-    if (st == ICQ_OK) {
-      e = cudaMemcpyAsync(ids_host, idd, ib, cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, sb, cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess && refine_host)
-        e = cudaMemcpyAsync(refine_host, rfd, rb, cudaMemcpyDeviceToHost, s);
-    }
-  }
-  cudaError_t e2 = cudaStreamSynchronize(s);
+  CUDA_TRY(cudaMemcpyAsync(qd, q_host, qb, cudaMemcpyHostToDevice, s));
+  const icq_status st =
+      search_impl(h, qd, nullptr, Q, k, sigma, flags, idd, scd, rfd, nullptr, nullptr, nullptr, ws,
+                  ws_bytes, s);  // (synchronises and checks the call's error word)
   if (st != ICQ_OK) return st;
+  cudaError_t e = cudaMemcpyAsync(ids_host, idd, ib, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scores_host, scd, sb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && refine_host)
+    e = cudaMemcpyAsync(refine_host, rfd, rb, cudaMemcpyDeviceToHost, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e2));
-  int32_t err = 0;
-  CUDA_TRY(cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost));
-  if (err & 1) return fail(ICQ_ERR_CUDA, "filter kernel shared-memory layout check failed");
   return ICQ_OK;
 }
 

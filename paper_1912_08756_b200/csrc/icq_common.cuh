@@ -183,6 +183,7 @@ struct WarpHeap {
   }
   __device__ __forceinline__ double top_e() const { return ue[0]; }
   __device__ __forceinline__ double top_f() const { return uf[0]; }
+  __device__ __forceinline__ int32_t top_i() const { return ui[0]; }
   __device__ __forceinline__ void replace_max(double xe, int32_t xid, double xf, int lane) {
     // 1. uniform top cache: drop entry 0, insert x if it ranks inside the prefix
     double le = ue[0];
@@ -233,6 +234,43 @@ struct WarpHeap {
   }
 };
 
+// --------------------------------------------------------------------------
+// The refinement threshold of search.py:149, `fast[i] < bound + sigma`, as a
+// float64 value t with the reference's test == `fast64 < t`.
+//
+// float64 sigma (a Python float / np.float64 argument, and index.sigma, which
+// data.py:252 stores as a Python float): t = bound + sigma, one float64 add.
+//
+// np.float32 sigma (sigma_f32, numpy >= 2 promotion rules, NEP 50): while the
+// heap maximum is a seed (id < k) its cached fast score is an np.float64
+// (search.py:141, indexing fast_all) and the sum stays float64.  Once it is an
+// inserted entry the cached score is a Python float (:153, from fast_list), so
+// `bound + sigma` is a float32 add of float32(bound), and the comparison
+// `fast_list[i] < np.float32` rounds fast_list[i] to float32 as well.
+// float32(x) < t32 <=> x < lb(t32), lb = the smallest double that rounds to a
+// float32 >= t32 (round-to-nearest-even is monotone).
+// --------------------------------------------------------------------------
+__device__ __forceinline__ double f32_lower_boundary(float t) {
+  if (!(t == t)) return (double)t;                 // NaN: every comparison false
+  if (t <= 0.f) return 0.0;                        // (fast >= 0) nothing rounds below 0
+  if (t == kInf) return 3.4028235677973366e38;     // 2^128 - 2^103 rounds to inf (tie, even)
+  const uint32_t b = __float_as_uint(t);
+  const double mid = ((double)__uint_as_float(b - 1u) + (double)t) * 0.5;  // exact
+  // a tie rounds to the even neighbour: mid itself rounds up to t iff t is even
+  return (b & 1u) ? __longlong_as_double(__double_as_longlong(mid) + 1) : mid;
+}
+__device__ __forceinline__ double live_thr(double bound, int32_t max_id, double sigma, int k,
+                                           bool f32) {
+  if (!f32 || max_id < k) return __dadd_rn(bound, sigma);
+  return f32_lower_boundary(__fadd_rn(__double2float_rn(bound), (float)sigma));
+}
+// an upper bound of live_thr over every bound <= b (both forms are monotone in b)
+__device__ __forceinline__ double thr_cover(double b, double sigma, bool f32, bool round_up) {
+  double t = round_up ? __dadd_ru(b, sigma) : __dadd_rn(b, sigma);
+  if (f32) t = fmax(t, f32_lower_boundary(__fadd_rn(__double2float_rn(b), (float)sigma)));
+  return t;
+}
+
 // Replay state (one warp; warp-uniform registers)
 struct Live {
   double T64, bound64, thr64;
@@ -241,15 +279,16 @@ struct Live {
   WarpHeap H;
 };
 
-__device__ __forceinline__ void live_update64(Live& L, double sigma) {
+__device__ __forceinline__ void live_update64(Live& L, double sigma, int k, bool f32) {
   L.T64 = L.H.top_e();
   L.bound64 = L.H.top_f();
-  L.thr64 = __dadd_rn(L.bound64, sigma);  // search.py:149 `bound + sigma`
+  L.thr64 = live_thr(L.bound64, L.H.top_i(), sigma, k, f32);  // search.py:149 `bound + sigma`
 }
 
 // + certified float32 thresholds of "fast64 < thr64"
-__device__ __forceinline__ void live_update(Live& L, int F, double sigma, bool wide) {
-  live_update64(L, sigma);
+__device__ __forceinline__ void live_update(Live& L, int F, double sigma, int k, bool f32,
+                                            bool wide) {
+  live_update64(L, sigma, k, f32);
   if (wide) {
     L.lo = -kInf;
     L.hi = kInf;
@@ -271,18 +310,20 @@ struct StaleThr {
   float lo, hi;
 };
 __device__ __forceinline__ StaleThr stale_core(double M, bool nan, double T, int F, double sigma,
-                                               double smin, bool wide) {
+                                               double smin, bool wide, bool f32) {
   StaleThr r{__longlong_as_double(0x7ff0000000000000LL), kInf, kInf};
   if (wide || nan) return r;
   double thr;
-  if (sigma == 0.0) {
+  if (sigma == 0.0 && !f32) {
     thr = M;
+  } else if (sigma == 0.0) {
+    thr = thr_cover(M, 0.0, true, false);
   } else {
     // (T - Smin) with float64 slack for the different summation orders of
     // fast and exact scores (relative 1e-12 >> K * 2^-53)
     const double ts = __dsub_ru(T, smin);
     const double u = fmax(M, __dadd_ru(ts, fabs(T) * 1e-12));
-    thr = __dadd_ru(u, sigma);
+    thr = thr_cover(u, sigma, f32, true);
   }
   if (!(thr == thr)) return r;
   r.thr = thr;
@@ -292,7 +333,7 @@ __device__ __forceinline__ StaleThr stale_core(double M, bool nan, double T, int
 // stale threshold from a heap array in shared memory (any order; entry 0 = maximum), one warp
 __device__ __forceinline__ StaleThr stale_from_heap(const double* he, const double* hf, int k,
                                                     int F, double sigma, double smin, bool wide,
-                                                    int lane) {
+                                                    bool f32, int lane) {
   double M = -__longlong_as_double(0x7ff0000000000000LL);
   bool nan = false;
   for (int i = lane; i < k; i += 32) {
@@ -302,7 +343,7 @@ __device__ __forceinline__ StaleThr stale_from_heap(const double* he, const doub
 #pragma unroll
   for (int o = 16; o; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
   nan = __any_sync(0xffffffffu, nan);
-  return stale_core(M, nan, he[0], F, sigma, smin, wide);
+  return stale_core(M, nan, he[0], F, sigma, smin, wide, f32);
 }
 
 __device__ __forceinline__ void record_survivor(uint32_t* surv, int64_t id) {

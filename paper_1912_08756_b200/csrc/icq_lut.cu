@@ -25,7 +25,7 @@ constexpr int kLutStack = 16;
 
 __global__ void __launch_bounds__(kLutTQ * kLutTJ) lut_build_kernel(
     const float* __restrict__ books, const double* __restrict__ q, double* __restrict__ lut,
-    int32_t KM, int32_t d, int32_t Q, const LutProg* __restrict__ prog) {
+    int32_t KM, int32_t d, int32_t Q, const LutProg* __restrict__ prog, int32_t* __restrict__ err) {
   __shared__ double sq[kLutTQ][kLeafMax];
   __shared__ float sc[kLutTJ][kLeafMax + 1];
 
@@ -49,10 +49,16 @@ __global__ void __launch_bounds__(kLutTQ * kLutTJ) lut_build_kernel(
     }
     const int L = prog->len[o];
     __syncthreads();
+    bool bad = false;
     for (int i = threadIdx.x; i < kLutTQ * L; i += blockDim.x) {
       const int r = i / L, t = i % L;
-      sq[r][t] = (q0 + r < Q) ? q[(size_t)(q0 + r) * d + start + t] : 0.0;
+      const double v = (q0 + r < Q) ? q[(size_t)(q0 + r) * d + start + t] : 0.0;
+      bad |= !isfinite(v);
+      sq[r][t] = v;
     }
+    // search.py:51-52: a non-finite query is a ValidationError (the first
+    // codeword tile reports it; the host turns it into ICQ_ERR_VALIDATION)
+    if (bad && blockIdx.x == 0 && err) atomicOr(err, 8);
     for (int i = threadIdx.x; i < kLutTJ * L; i += blockDim.x) {
       const int r = i / L, t = i % L;
       sc[r][t] = (j0 + r < KM) ? books[(size_t)(j0 + r) * d + start + t] : 0.f;
@@ -119,10 +125,10 @@ bool make_lut_prog(int d, LutProg* out) {
 }
 
 cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, int m, int d,
-                       int Q, const LutProg* prog_dev, cudaStream_t s) {
+                       int Q, const LutProg* prog_dev, int32_t* err, cudaStream_t s) {
   const int KM = K * m;
   dim3 grid((KM + kLutTJ - 1) / kLutTJ, (Q + kLutTQ - 1) / kLutTQ);
-  lut_build_kernel<<<grid, kLutTQ * kLutTJ, 0, s>>>(books, q, lut, KM, d, Q, prog_dev);
+  lut_build_kernel<<<grid, kLutTQ * kLutTJ, 0, s>>>(books, q, lut, KM, d, Q, prog_dev, err);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,7 @@
 // Every decision compares the reference's float64 values, so ids, scores,
 // refinement counts and survivor sets are bitwise the reference's.
 #pragma once
+#include <mutex>
 #include <type_traits>
 
 #ifndef ICQ_PREFETCH_TILES
@@ -45,7 +46,6 @@
 namespace icq {
 
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr int kSelectJ = 40;  // prologue: budgeted prefilter only for budgets below this
 
 // --------------------------------------------------------------------------
 // decision context shared by the prologue and replay warps
@@ -54,12 +54,11 @@ struct RCtx {
   const double* lut;  // float64 LUT [K][m] in shared memory
   const uint8_t* codes_full;
   const uint8_t* fb;  // fast books
-  int KP, m, K, F;
+  int KP, m, K, F, k;
   double sigma;
+  bool f32;  // numpy float32-sigma promotion (live_thr)
   bool pw, wide;
   uint32_t* surv;
-  int64_t ins_limit;     // the filter threshold holds up to this many insertions
-  int64_t* stop_pos;     // shared: first undecided item when the budget ran out
 };
 
 struct Decided {
@@ -175,6 +174,24 @@ static __device__ double smin_rd(const double* lut, int K, int m, const uint8_t*
 // ==========================================================================
 // K2: prologue
 // ==========================================================================
+// max fast score over the J+1 largest-exact heap entries (he/hf sorted
+// descending by (exact, id): entries 0..J), warp-wide; *arg = its entry
+__device__ __forceinline__ double heap_AJ(const double* hf, int k, int J, int lane, int* arg) {
+  const int top = min(k, J + 1);
+  double A = -kInf64;
+  int ai = 0;
+  for (int i = lane; i < top; i += 32)
+    if (hf[i] > A) { A = hf[i]; ai = i; }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double oA = __shfl_xor_sync(kFull, A, o);
+    const int oi = __shfl_xor_sync(kFull, ai, o);
+    if (oA > A || (oA == A && oi < ai)) { A = oA; ai = oi; }
+  }
+  if (arg) *arg = ai;
+  return A;
+}
+
 template <int FP>
 __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __grid_constant__ PipeParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
@@ -182,6 +199,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   const int q = blockIdx.x;
   const int K = p.K, m = p.m, F = p.F, k = p.k;
   const int64_t n = p.n;
+  const bool f32s = p.sigma_f32 != 0;
   const ProLayout Ly = pro_layout(K, m, F, k);
   double* lut = reinterpret_cast<double*>(dsm + Ly.lut64);
   float* lut32 = reinterpret_cast<float*>(dsm + Ly.lut32);
@@ -196,13 +214,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   volatile float* pub_hi = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 68);
   volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctrl + 72);
   volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctrl + 80);
+  int* nL_total = reinterpret_cast<int*>(dsm + Ly.ctrl + 92);  // block items under the list bound
   int* band_total = reinterpret_cast<int*>(dsm + Ly.ctrl + 96);  // near-ties seen by the prefilter
-  volatile int* ins_recent = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 100);  // last 4 blocks
-  volatile int* pub_J = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 104);  // prefilter budget
-  volatile long long* cut = reinterpret_cast<volatile long long*>(dsm + Ly.ctrl + 112);  // pass end
-  volatile float* pub_hiM = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 120);  // M's float32 hi
-  volatile int* final_J = reinterpret_cast<volatile int*>(dsm + Ly.ctrl + 124);      // budget at stop
-  int* nM_total = reinterpret_cast<int*>(dsm + Ly.ctrl + 92);  // block items under M (stop rule)
+  volatile float* pub_hiL = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 120);  // list bound hi
   const long long t0 = clock64();
 
   // 1. float64 LUT -> smem, float32 copy of the fast books (prefilter)
@@ -223,8 +237,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   c.lut = lut;
   c.codes_full = p.codes_full;
   c.fb = p.fast_books;
-  c.KP = p.KP; c.m = m; c.K = K; c.F = F;
+  c.KP = p.KP; c.m = m; c.K = K; c.F = F; c.k = k;
   c.sigma = p.sigma;
+  c.f32 = f32s;
   c.pw = n == 1;  // numpy row-sum order, see ref_row_sum
   c.wide = wide;
   c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
@@ -266,20 +281,24 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
   __syncthreads();
 
+  // the list threshold theta the filter would get if the prologue ended here
+  // (A_J + sigma over the current heap, sorted descending by (exact, id))
+  auto list_theta = [&](int lane_) -> double {
+    const double A = heap_AJ(hf, k, p.list_j, lane_, nullptr);
+    return thr_cover(A, p.sigma, f32s, false);
+  };
   int64_t refinements = 0, insertions = 0;
   double smin = 0.0;
   if (warp == 0) {
     smin = p.sigma == 0.0 ? 0.0 : smin_rd(lut, K, m, p.fast_books, F, lane);
-    const StaleThr t = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
+    const StaleThr t = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, f32s, lane);
+    float lL = kInf, hL = kInf;
+    certified_bounds(list_theta(lane), F, lL, hL);
     if (lane == 0) {
       *pub_lo = t.lo; *pub_hi = t.hi; *pub_thr = t.thr; *flag = k < n ? 1 : 0;
       *band_total = 0;
-      *ins_recent = 0;
-      *pub_J = kInfBudget;
-      *cut = -1;
-      *pub_hiM = t.hi;
-      *final_J = kInfBudget;
-      *nM_total = 0;
+      *pub_hiL = p.pro_live ? hL : t.hi;
+      *nL_total = 0;
     }
   }
   __syncthreads();
@@ -299,7 +318,6 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   int64_t pro_cand = 0;
   long long tp[3] = {0, 0, 0};
   int64_t nblocks = 0;
-  int ins_hist[4] = {0, 0, 0, 0};  // thread 0: insertions of the last four blocks
   while (*flag) {
     const long long ta = clock64();
     ++nblocks;
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     const int64_t bend = min(n, base + kProBlock);
     const float h = *pub_hi, hl = *pub_lo;
     const double hthr = *pub_thr;
-    const float hM = *pub_hiM;
+    const float hL = *pub_hiL;
     // 3a. fp32 prefilter of 8 consecutive items per thread (codes_fast rows)
     const int64_t i0 = base + (int64_t)tid * 8;
     uint32_t w[2 * FP];
@@ -329,7 +347,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     }
     uint32_t mask = 0;
     int nband = 0;  // items float32 could not decide (near / exact ties with the threshold)
-    int nm = 0;     // items under M's float32 bound (how loose the unbudgeted filter would be)
+    int nl = 0;     // items under the list bound (how long the filter's lists would be)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float x = 0.f;
@@ -353,11 +371,11 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
         cand = d < hthr;
       }
       mask |= ((i >= pos) & (i < bend) & cand) ? (1u << j) : 0u;
-      nm += (i >= pos) & (i < bend) & (x < hM);
+      nl += (i >= pos) & (i < bend) & (x < hL);
     }
     // 3b. ordered compaction (thread order = item order)
     if (nband) atomicAdd(band_total, nband);
-    if (nm) atomicAdd(nM_total, nm);
+    if (nl) atomicAdd(nL_total, nl);
     const int cnt = __popc(mask);
     int incl = cnt;
 #pragma unroll
@@ -407,12 +425,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     //     prefix (the bound moves there); the lanes after it are re-tested
     //     against the new bound.  The heap is the sorted-array WarpHeap.
     if (warp == 0) {
-      const int64_t ins_before = insertions;
-      const int64_t ins_limit = *pub_J >= kInfBudget ? INT64_MAX : insertions + *pub_J;
-      long long cut_id = -1;
       double T = H.top_e();
-      double thr = __dadd_rn(H.top_f(), p.sigma);
-      for (int c0 = 0; c0 < ncand && cut_id < 0; c0 += 32) {
+      double thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
+      for (int c0 = 0; c0 < ncand; c0 += 32) {
         const int ci = c0 + lane;
         const bool ok = ci < ncand;
         const double fv = ok ? cf[ci] : 0.0;
@@ -436,174 +451,89 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
           const int32_t nid = __shfl_sync(kFull, id, first);
           H.replace_max(ne, nid, nf, lane);
           T = H.top_e();
-          thr = __dadd_rn(H.top_f(), p.sigma);
+          thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
           ++insertions;
-          if (insertions > ins_limit) {  // the prefilter threshold is spent: re-filter the rest
-            cut_id = (long long)nid + 1;
-            break;
-          }
         }
       }
-      H.store(lane);  // smem copy for the threshold below and the hand-off
-      if (lane == 0) {
-        *cut = cut_id;
-        ins_hist[nblocks & 3] = (int)(insertions - ins_before);
-        *ins_recent = ins_hist[0] + ins_hist[1] + ins_hist[2] + ins_hist[3];
-      }
+      H.store(lane);  // smem copy for the thresholds below and the hand-off
     }
     __syncwarp();
     if (warp == 0) {
-      StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, lane);
-      const float hiM_next = tn.hi;  // M's bound for the next block's count
-      // insertions have become rare: prefilter (and later filter) with the
-      // budgeted A_J (max fast over the J+1 largest-exact entries), far
-      // tighter than M when a high-fast item sits deep in the heap
-      const int Jc = (*ins_recent) * 2;  // 0 once insertions have stopped: A_0 = the live bound
-      int Jpub = kInfBudget;
-      if (p.max_rounds > 1 && p.sigma == 0.0 && !wide && nblocks >= 4 && Jc < kSelectJ &&
-          Jc < k - 1) {
-        double A = -__longlong_as_double(0x7ff0000000000000LL), A0 = 0.0;
-        double pe = __longlong_as_double(0x7ff0000000000000LL);
-        int32_t pi = 0x7fffffff;
-        int Jt = 0;
-        for (int r = 0; r <= Jc; ++r) {  // r-th largest (exact, id): warp argmax below the last
-          double be = -__longlong_as_double(0x7ff0000000000000LL), bf = 0.0;
-          int32_t bi = -1;
-          for (int i = lane; i < k; i += 32) {
-            const double e2 = he[i];
-            const int32_t i2 = hi[i];
-            if (key_gt(pe, pi, e2, i2) && (bi < 0 || key_gt(e2, i2, be, bi))) { be = e2; bi = i2; bf = hf[i]; }
-          }
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const double oe = __shfl_xor_sync(kFull, be, o);
-            const int32_t oi = __shfl_xor_sync(kFull, bi, o);
-            const double of = __shfl_xor_sync(kFull, bf, o);
-            if (oi >= 0 && (bi < 0 || key_gt(oe, oi, be, bi))) { be = oe; bi = oi; bf = of; }
-          }
-          pe = be;
-          pi = bi;
-          if (r == 0) A0 = bf;
-          else if (fmax(A, bf) > A0 * (1.0 + p.budget_slack)) break;  // stay near the live bound
-          A = fmax(A, bf);
-          Jt = r;
-        }
-        if (A < tn.thr) {
-          tn.thr = A;
-          certified_bounds(A, F, tn.lo, tn.hi);
-          Jpub = Jt;
-        }
-      }
-      const bool stopped = *cut >= 0;
-      const int64_t pend = stopped ? (int64_t)*cut : bend;
-      const int64_t nb = pend - max(pos, base);
-      bool more = pend < n && pend < p.pro_max;
-      // stop once the filter's threshold passes <= 1/pro_div of a block: M
-      // itself (unbudgeted), or the budgeted A_J the prefilter just used
-      const bool under_budget = *pub_J < kInfBudget;  // this block's prefilter threshold
-      int fj = kInfBudget;  // budget the filter gets (also when the length cap ends it)
-      if (under_budget) fj = *pub_J;
-      if (!stopped && bend >= p.pro_min) {
-        // (under M the prefilter count is exact: near-ties were resolved in float64)
-        const int64_t nM = under_budget ? (int64_t)(*nM_total) : (int64_t)ncand;
-        if (nM * p.pro_div <= nb) {
-          more = false;
-          fj = kInfBudget;
-        } else if (under_budget && (int64_t)ncand * p.pro_div <= nb && nM * p.pro_div > 16 * nb) {
-          more = false;  // M is grossly loose, the budgeted A_J is not: rounds pay off
-        }
+      const StaleThr tn = stale_from_heap(he, hf, k, F, p.sigma, smin, wide, f32s, lane);
+      // the heap array is sorted descending by (exact, id) (WarpHeap.store)
+      float lL = kInf, hLn = kInf;
+      if (p.pro_live) certified_bounds(list_theta(lane), F, lL, hLn);
+      const int64_t nb = bend - max(pos, base);
+      bool more = bend < n && bend < p.pro_max;
+      // stop once the filter's lists would be short: the block's items under
+      // the list bound theta (pro_live) or under the stale M are <= 1/pro_div
+      if (bend >= p.pro_min) {
+        const int64_t nX = p.pro_live ? (int64_t)(*nL_total) : (int64_t)ncand;
+        if (nX * p.pro_div <= nb) more = false;
       }
       if (lane == 0) {
-        *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr; *pub_J = Jpub;
-        *pub_hiM = hiM_next;
-        *final_J = fj;
-        *nM_total = 0;
+        *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr;
+        *pub_hiL = p.pro_live ? hLn : tn.hi;
+        *nL_total = 0;
         *flag = more ? 1 : 0;
       }
     }
     __syncthreads();
-    pos = *cut >= 0 ? (int64_t)*cut : bend;
+    pos = bend;
     tp[0] += tb - ta;
     tp[1] += tc - tb;
     tp[2] += clock64() - tc;
   }
 
   // 4. hand the state to the filter / replay kernels: the heap sorted
-  //    descending by (exact, id) (rank sort through the candidate buffers)
+  //    descending by (exact, id) (WarpHeap.store keeps the array sorted), and
+  //    the list threshold theta = A_J + sigma (A_J: max fast over the J+1
+  //    largest-exact entries; J = 0 makes theta the live threshold itself).
+  //    The filter lists every later item with fast < theta; the replay walks
+  //    the database in order wherever the live threshold rises above theta.
   __syncthreads();
-  for (int i = tid; i < k; i += kProThreads) {
-    int rank = 0;
-    for (int j = 0; j < k; ++j) rank += key_gt(he[j], hi[j], he[i], hi[i]) ? 1 : 0;
-    ce[rank] = he[i];
-    cf[rank] = hf[i];
-    cid[rank] = hi[i];
-  }
-  __syncthreads();
-  for (int i = tid; i < k; i += kProThreads) {
-    he[i] = ce[i];
-    hf[i] = cf[i];
-    hi[i] = cid[i];
-  }
-  __syncthreads();
-  if (tid == 0) {
-    // The filter threshold for the rest of the database.  sigma == 0: A_J =
-    // max fast over the J+1 largest-exact heap entries bounds the live bound
-    // for the next J insertions (they evict entries in exact order; an
-    // inserted item has fast < bound), so with J sized from the recent
-    // insertion rate it is far tighter than M = A_{k-1} when a high-fast item
-    // sits deep in the heap.  The replay stops when the budget runs out and
-    // the next round re-filters the rest.  sigma > 0: U + sigma, unbudgeted.
-    int J = p.j0 >= 0 ? p.j0 : *final_J;  // the budget the prologue stopped under (M: none)
-    int best = -1;
-    double thr = *pub_thr;
-    float flo = *pub_lo, fhi = *pub_hi;
-    if (p.max_rounds <= 1) J = kInfBudget;  // single round: M, valid for every later item
-    if (!wide && p.sigma == 0.0) {
-      if (J >= k - 1) J = kInfBudget;
-      const int top = J == kInfBudget ? k : J + 1;
-      best = 0;
-      for (int i = 1; i < top; ++i)
-        if (hf[i] > hf[best]) best = i;
-      thr = hf[best];
-      certified_bounds(thr, F, flo, fhi);
-    } else {
-      J = kInfBudget;
-    }
+  if (warp == 0) {
+    int best = 0;
+    const double A = heap_AJ(hf, k, p.list_j, lane, &best);
+    double thr = wide ? kInf64 : thr_cover(A, p.sigma, f32s, false);
+    float flo = kInf, fhi = kInf;
+    if (!wide) certified_bounds(thr, F, flo, fhi);
     // tie rejection costs the filter a tuple compare per candidate: enabled
     // only where the prologue saw near-ties in bulk (few-codeword books);
     // items with the threshold item's fast-code tuple tie at thr exactly
     const bool ties = (int64_t)(*band_total) * 2048 > pos && !(p.debug & 1);
-    const bool ok = ties && FP <= 8 && best >= 0;
+    const bool ok = ties && FP <= 8 && p.sigma == 0.0 && !f32s && !wide;
     uint2 tup = make_uint2(0u, 0u);
-    if (ok) {
+    if (ok && lane == 0) {
       const Row r = load_fast_row(p.codes_fast, FP, hi[best]);
       tup = make_uint2(r.w[0], r.w[1]);
     }
-    QState st;
-    st.P = pos;
-    st.refinements = refinements;
-    st.insertions = insertions;
-    st.pro_cand = pro_cand;
-    st.pro_cycles = clock64() - t0;
-    st.pro_t[0] = tp[0];
-    st.pro_t[1] = tp[1];
-    st.pro_t[2] = tp[2];
-    st.pro_t[3] = nblocks;
-    st.hi = fhi;
-    st.lo = flo;
-    st.thr = thr;
-    st.mtup[0] = tup.x;
-    st.mtup[1] = tup.y;
-    st.mt_valid = ok ? 1 : 0;
-    st.wide = wide ? 1 : 0;
-    st.ovf_pages = 0;
-    st.ovf_pool = 0;
-    st.skipped = 0;
-    st.J = J;
-    st.ins0 = insertions;
-    st.done = 0;
-    st.rounds = 0;
-    p.qs[q] = st;
+    if (lane == 0) {
+      QState st;
+      st.P = pos;
+      st.refinements = refinements;
+      st.insertions = insertions;
+      st.pro_cand = pro_cand;
+      st.pro_cycles = clock64() - t0;
+      st.pro_t[0] = tp[0];
+      st.pro_t[1] = tp[1];
+      st.pro_t[2] = tp[2];
+      st.pro_t[3] = nblocks;
+      st.hi = fhi;
+      st.lo = flo;
+      st.thr = thr;
+      st.mtup[0] = tup.x;
+      st.mtup[1] = tup.y;
+      st.mt_valid = ok ? 1 : 0;
+      st.wide = wide ? 1 : 0;
+      st.done = 0;
+      st.rounds = 0;
+      st.walked = 0;
+      st.ovf_pages = 0;
+      st.ovf_pool = 0;
+      st.skipped = 0;
+      p.qs[q] = st;
+    }
   }
   for (int i = tid; i < k; i += kProThreads) {
     p.heap_e[(size_t)q * k + i] = he[i];
@@ -650,15 +580,14 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
 
-  if (p.round > 0 && *(volatile int32_t*)&p.active[p.round - 1] == 0) return;  // all finished
   const int K = p.K, m = p.m, F = p.F;
   const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
   const int64_t U = (int64_t)p.Q * p.NR;
   int64_t u0, u1, ustep;
-  const bool rmaj = p.range_major || p.round > 0;
+  const bool rmaj = p.range_major != 0 || p.round > 0;
   const bool rmaj_stream = p.range_major != 0;
-  if (rmaj) {  // all CTAs sweep the ranges together: codes reused in L2, and in later
-               // rounds the few unfinished queries spread over all SMs
+  if (rmaj) {  // all CTAs sweep the ranges together: codes reused in L2 (and in later
+               // rounds the few unfinished queries spread over all SMs)
     u0 = blockIdx.x; u1 = U; ustep = gridDim.x;
   } else {     // contiguous unit blocks: one query's LUT serves many units
     u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1;
@@ -938,20 +867,23 @@ __device__ __forceinline__ double entry_f64(uint2 tail, const double* lutf, int 
 }
 
 // Decide one window of up to kWU*32 items in database order (u-major, then
-// lane), each with its float32 fast score and tuple.  Refined items (fast <
-// bound + sigma, search.py:149: certified float32 test, exact float64 from
-// the tuple in the uncertain band) are compacted in order, their exact
-// scores computed 32 at a time, and the first one under the heap maximum is
+// lane), each with its float64-decidable fast-code tuple (or float64 fast
+// score, FP = 16) and, when known, its exact score.  Refined items (fast <
+// bound + sigma, search.py:149) are compacted in order, their exact scores
+// computed 32 at a time, and the first one under the heap maximum is
 // inserted (search.py:152-154).  An insertion moves the bound (up or down):
 // when it rises, the items after the insertion are compacted again.
+// Returns -1 when the whole window is decided, else the window position
+// (u * 32 + lane) of the insertion after which the live threshold left
+// (floor_, cap]: above cap (the caller's list / pre-filter no longer covers
+// the items after it) or at most floor_ (a walk may hand back to the lists).
 template <int FP>
-__device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
-                                              const int32_t (&ids)[kWU], const float (&f32)[kWU],
-                                              const uint2 (&tail)[kWU], const double (&ex)[kWU],
-                                              const bool (&valid)[kWU], int32_t* sid,
-                                              int32_t* sidx, double* sfv, double* sfe,
-                                              const double* lutf, double cap = __builtin_huge_val(),
-                                              int* brk = nullptr) {
+__device__ __forceinline__ int replay_window(Live& L, const RCtx& c, int lane,
+                                             const int32_t (&ids)[kWU], const uint2 (&tail)[kWU],
+                                             const double (&ex)[kWU], const bool (&valid)[kWU],
+                                             int32_t* sid, int32_t* sidx, double* sfv,
+                                             double* sfe, const double* lutf, double cap,
+                                             double floor_) {
   int pos0 = 0;  // first undecided window position (u * 32 + lane)
   const uint32_t lt = (1u << lane) - 1u;
   for (;;) {
@@ -962,7 +894,7 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
     int tot = 0;
 #pragma unroll
     for (int u = 0; u < kWU; ++u) {
-      bool cand = valid[u] && (u * 32 + lane >= pos0);  // (f32 is -inf for every caller)
+      bool cand = valid[u] && (u * 32 + lane >= pos0);
       d[u] = 0.0;
       if (cand) {
         d[u] = entry_f64<FP>(tail[u], lutf, c.m, c.F);
@@ -972,7 +904,7 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
       base[u] = tot;
       tot += __popc(lm[u]);
     }
-    if (tot == 0) return false;
+    if (tot == 0) return -1;
 #pragma unroll
     for (int u = 0; u < kWU; ++u) {
       if ((lm[u] >> lane) & 1u) {
@@ -1010,17 +942,12 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
         const double nf = __shfl_sync(kFull, f64, first);
         const int32_t nid = __shfl_sync(kFull, id, first);
         L.H.replace_max(ne, nid, nf, lane);
-        live_update64(L, c.sigma);  // (the replay never uses the float32 bounds)
+        live_update64(L, c.sigma, c.k, c.f32);  // (the replay never uses the float32 bounds)
         ++L.insertions;
-        if (L.insertions > c.ins_limit) {  // budget spent: later lists may be incomplete
-          if (lane == 0) *c.stop_pos = (int64_t)nid + 1;
+        if (L.thr64 > cap || L.thr64 <= floor_) {
+          const int r = __shfl_sync(kFull, wpos, first);
           __syncwarp();
-          return true;
-        }
-        if (brk && L.thr64 > cap) {  // bound rose above the caller's pre-filter: it walks on
-          *brk = __shfl_sync(kFull, wpos, first);
-          __syncwarp();
-          return false;
+          return r;
         }
         if (L.thr64 > thr) {  // bound rose: re-compact everything after the insertion
           pos0 = __shfl_sync(kFull, wpos, first) + 1;
@@ -1030,7 +957,7 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
       }
     }
     __syncwarp();
-    if (!restart) return false;
+    if (!restart) return -1;
   }
 }
 
@@ -1040,9 +967,21 @@ __device__ __forceinline__ bool replay_window(Live& L, const RCtx& c, int lane,
 // is staged by cp.async, chunk c+1 prepared (float64 fast score from the
 // tuple; exact score of every entry refined under the bound warp 0 last
 // published) and chunk c decided, all at once, one CTA barrier per chunk.
+//
+// The lists hold every item with fast < theta (the list threshold the
+// prologue chose).  They decide the reference loop exactly while the live
+// threshold bound + sigma stays <= theta.  When an insertion lifts it above
+// theta, the CTA WALKS the database in order from the next item: all four
+// warps flag 64k-item sub-ranges against the live threshold (float64 fast
+// scores from the codes), warp 0 decides the flagged items, and the walk
+// hands back to the lists at the first insertion that brings the threshold
+// back to <= theta.  Slices whose candidates overflowed their pages are
+// walked the same way (without the early hand-back).
 constexpr int kRW = 4;            // warps per replay CTA
 constexpr int kRP = (kRW - 1) * 32;  // preparing threads
-constexpr int kMaxChunks = 512;   // chunk descriptors per slice group
+constexpr int kMaxChunks = 512;   // chunk descriptors per slice group (kSG * kMaxPages * kPG / kCH)
+static_assert(kSG * ((kMaxPages * kPG + kCH - 1) / kCH) <= kMaxChunks,
+              "a slice group always fits the chunk descriptors");
 
 template <int FP>
 __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_constant__ PipeParams p) {
@@ -1067,12 +1006,17 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   uint4* ring = reinterpret_cast<uint4*>(dsm + Ly.ring);
   double* ring_e = reinterpret_cast<double*>(dsm + Ly.ringe);
   int32_t* plist = reinterpret_cast<int32_t*>(dsm + Ly.plist);   // prep: live-ish entries
+  // control words: [0] chunks, [1] dropped entries, [2] prep list count,
+  // [3] walk request, [13] stopped for the next round, [14] re-run the
+  // chunk, [15] walk handed back
   volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctl);
   volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctl + 16);
+  volatile long long* walk_from = reinterpret_cast<volatile long long*>(dsm + Ly.ctl + 24);
+  volatile double* tsub = reinterpret_cast<volatile double*>(dsm + Ly.ctl + 32);
+  volatile long long* snext = reinterpret_cast<volatile long long*>(dsm + Ly.ctl + 40);
+  volatile long long* sskip = reinterpret_cast<volatile long long*>(dsm + Ly.ctl + 48);
   const long long t0 = clock64();
   const QState st = p.qs[q];
-  if (st.done) return;  // finished in an earlier round
-  int64_t* stop_pos = reinterpret_cast<int64_t*>(dsm + Ly.ctl + 24);
   for (int i = tid; i < k; i += kRW * 32) {
     he[i] = p.heap_e[(size_t)q * k + i];
     hf[i] = p.heap_f[(size_t)q * k + i];
@@ -1086,6 +1030,11 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       lutf[i] = glut[p.fast_books[s2] * m + j];
     }
   }
+  if (st.done) return;  // finished in an earlier round
+  if (tid == 0) {
+    ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[13] = 0; ctl[14] = 0; ctl[15] = 0;
+    *sskip = st.P - 1;
+  }
   __syncthreads();
   Live L;
   L.refinements = st.refinements;
@@ -1096,31 +1045,161 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   L.H.he = he;
   L.H.hf = hf;
   L.H.hi = hi;
-  int64_t fallback_slices = 0, listed = 0;
+  int64_t fallback_slices = 0, listed = 0, walked = 0;
   long long t_work = 0, t_wait = 0;  // warp 0: deciding vs waiting at the chunk barrier
   RCtx c;
   c.lut = lut;
   c.codes_full = p.codes_full;
   c.fb = p.fast_books;
-  c.KP = p.KP; c.m = m; c.K = K; c.F = F;
+  c.KP = p.KP; c.m = m; c.K = K; c.F = F; c.k = k;
   c.sigma = p.sigma;
+  c.f32 = p.sigma_f32 != 0;
   c.pw = false;  // n >= 2 whenever the replay runs (P >= k >= 1 and P < n)
   c.wide = false;
   c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
-  c.ins_limit = st.J >= kInfBudget ? INT64_MAX : st.ins0 + st.J;
-  c.stop_pos = stop_pos;
-  if (tid == 0) { ctl[3] = 0; *stop_pos = n; }
+  const double theta = st.thr;  // the lists' threshold
+  const int64_t SW = p.RS / kFW;
+
+  // ---- the in-order walk (all threads; CTA-uniform control) ----------------
+  auto fast_at = [&](int64_t i, uint2& tup) -> double {
+    const Row r2 = load_fast_row(p.codes_fast, FP, i);
+    double x;
+    if constexpr (FP <= 8) {
+      tup = make_uint2(r2.w[0], r2.w[1]);
+      x = tuple_f64<FP>(tup, lutf, m, F);
+    } else {
+      x = 0.0;  // float64 fast score in the reference's order
+#pragma unroll
+      for (int s2 = 0; s2 < FP; ++s2)
+        if (s2 < F) x = __dadd_rn(x, lutf[s2 * m + (int)r2.byte(s2)]);
+      const unsigned long long db = (unsigned long long)__double_as_longlong(x);
+      tup = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
+    }
+    return x;
+  };
+  // warp 0: decide the items at positions [0, npos) given by position -> id
+  auto decide_items = [&](auto id_at, int npos, double cap, double floor_) -> int {
+    for (int w0 = 0; w0 < npos; w0 += kWU * 32) {
+      int32_t ids2[kWU];
+      uint2 t2[kWU];
+      double e2[kWU];
+      bool valid2[kWU];
+#pragma unroll
+      for (int u = 0; u < kWU; ++u) {
+        const int x = w0 + u * 32 + lane;
+        valid2[u] = x < npos;
+        const int64_t i = valid2[u] ? id_at(x) : 0;
+        ids2[u] = (int32_t)i;
+        t2[u] = make_uint2(0u, 0u);
+        e2[u] = __longlong_as_double(0x7ff8000000000000LL);
+        if (valid2[u]) (void)fast_at(i, t2[u]);
+      }
+      const int b = replay_window<FP>(L, c, lane, ids2, t2, e2, valid2, sid, sidx, sfv, sfe,
+                                      lutf, cap, floor_);
+      if (b >= 0) return w0 + b;
+    }
+    return -1;
+  };
+  // Walk items [from, to) in order with the live threshold.  hand_back: stop
+  // at the first insertion that brings the threshold back to <= theta (the
+  // lists cover the rest).  Afterwards *sskip = the last decided item.
+  // Scratch: rmask holds sub/32 flag words, rlst 1024 positions.
+  auto walk = [&](int64_t from, int64_t to, bool hand_back, uint32_t* rmask, int32_t* rlst,
+                  int sub) {
+    const int kSub = sub;  // items per flagged sub-range
+    int64_t s0 = from;
+    bool back = false;
+    while (s0 < to && !back) {
+      const int64_t s1 = min(to, s0 + (int64_t)kSub);
+      const int nsub = (int)(s1 - s0);
+      if (tid == 0) *tsub = (p.debug & 16) ? kInf64 : L.thr64;  // debug: flag every item
+      __syncthreads();
+      const double T = *tsub;
+      constexpr int kPW = 16;
+      // kPW words per warp and pass: the row reads of a pass overlap
+      for (int b0 = warp * 32 * kPW; b0 < nsub; b0 += kRW * 32 * kPW) {
+        Row rows[kPW];
+#pragma unroll
+        for (int u = 0; u < kPW; ++u) {
+          const int x = b0 + u * 32 + lane;
+          if (x < nsub) rows[u] = load_fast_row(p.codes_fast, FP, s0 + x);
+        }
+#pragma unroll
+        for (int u = 0; u < kPW; ++u) {
+          const int x = b0 + u * 32 + lane;
+          bool under = false;
+          if (x < nsub) {
+            double f = 0.0;  // float64 fast score in the reference's order
+#pragma unroll
+            for (int s2 = 0; s2 < FP; ++s2)
+              if (s2 < F) f = __dadd_rn(f, lutf[s2 * m + (int)rows[u].byte(s2)]);
+            under = !(f >= T);  // (T = inf: every item, NaN scores included)
+          }
+          const uint32_t bw = __ballot_sync(kFull, under);
+          if (lane == 0 && b0 + u * 32 < nsub) rmask[(b0 >> 5) + u] = bw;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        int64_t next = s1;
+        bool hb = false;
+        const int nwords = (nsub + 31) >> 5;
+        for (int w0 = 0; w0 < nwords; w0 += 32) {
+          const uint32_t wv = w0 + lane < nwords ? rmask[w0 + lane] : 0u;
+          const int cw = __popc(wv);
+          int incl = cw;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int nl = __shfl_sync(kFull, incl, 31);
+          int o = incl - cw;
+          for (uint32_t bb = wv; bb; bb &= bb - 1) rlst[o++] = (w0 + lane) * 32 + __ffs(bb) - 1;
+          __syncwarp();
+          const int b = decide_items([&](int x) { return s0 + rlst[x]; }, nl, T,
+                                     hand_back ? theta : -kInf64);
+          __syncwarp();
+          if (b >= 0) {  // an insertion moved the threshold out of (floor, T]
+            const int64_t y = s0 + rlst[b];
+            hb = hand_back && L.thr64 <= theta;
+            next = hb ? y : y + 1;  // rose above T: flag again from the next item
+            break;
+          }
+        }
+        if (lane == 0) {
+          *snext = (long long)next;
+          ctl[15] = hb ? 1 : 0;
+          *pub_thr = L.thr64;
+        }
+      }
+      __syncthreads();
+      back = ctl[15] != 0;
+      const int64_t nx = (int64_t)*snext;
+      if (tid == 0) walked += (back ? nx + 1 : nx) - s0;
+      s0 = back ? nx + 1 : nx;
+      // a long walk is handed to the next round: the filter lists the rest
+      // under the current live threshold on all SMs (one CTA walks ~1 item
+      // per clock; a filter pass streams the whole query in microseconds)
+      if (hand_back && !back && !p.last_round && s0 < to && s0 - from > p.walk_cap) {
+        if (tid == 0) ctl[13] = 1;
+        break;
+      }
+    }
+    if (tid == 0) *sskip = (long long)((back || ctl[13]) ? s0 - 1 : max(to - 1, (int64_t)*sskip));
+    __syncthreads();
+  };
+
   if (st.P < n) {
     if (warp == 0) {
       L.H.load(lane);
-      live_update(L, F, p.sigma, false);
+      live_update(L, F, p.sigma, k, c.f32, false);
       if (lane == 0) *pub_thr = L.thr64;
     }
-    const int64_t SW = p.RS / kFW;
     const int NS = p.NR * kFW;  // slices of this query, in database order
     const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
     const int ptid = tid - 32;  // preparing thread index (warps 1..3)
-    for (int g0 = 0; g0 < NS; g0 += kSG) {
+    for (int g0 = 0; g0 < NS && *sskip < n - 1 && !ctl[13]; g0 += kSG) {
       const int ng = min(kSG, NS - g0);
       {  // group meta (counts + page ids) -> shared memory
         const int pieces = ng * kSliceInts / 4;
@@ -1135,12 +1214,13 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       if (tid == 0) {
         // scum: listed entries before each slice (rescans count 0); chunks:
         // {first virtual entry, length, -1} or {-, -, rescan slice}
-        int acc = 0, nc = 0, open = -1;
+        int acc = 0, nc = 0, open = -1, dropped = 0;
         for (int t2 = 0; t2 < ng; ++t2) {
           scum[t2] = acc;
           const int cnt = smeta[t2 * kSliceInts];
           if (cnt < 0) {
             if (nc < kMaxChunks) { chunk[3 * nc] = acc; chunk[3 * nc + 1] = 0; chunk[3 * nc + 2] = t2; ++nc; }
+            else dropped = 1;
             open = -1;
             continue;
           }
@@ -1158,15 +1238,16 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             acc += take;
             rem -= take;
           }
+          dropped |= rem > 0;
         }
         scum[ng] = acc;
         ctl[0] = nc;
-        ctl[1] = nc >= kMaxChunks ? 1 : 0;
+        ctl[1] = dropped;
       }
       __syncthreads();
       const int nc = ctl[0];
-      if (ctl[1]) {  // more chunks than descriptors: should not happen (kMaxChunks * kCH entries)
-        if (tid == 0) atomicExch(p.error, 4);
+      if (ctl[1]) {  // cannot happen (static_assert above): fail loudly, never silently
+        if (tid == 0) atomicOr(p.error, 4);
         break;
       }
       listed += scum[ng];
@@ -1210,6 +1291,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         double* ex = ring_e + (ch % kRSlots) * kCH;
         const int len = chunk[3 * ch + 1];
         const double thr = *pub_thr;
+        const int64_t skp = (int64_t)*sskip;
         for (int i = ptid; i < len; i += kRP) {
           uint4 ent = src[i];
           const double f = entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F);
@@ -1218,14 +1300,13 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           ent.w = (uint32_t)(fb >> 32);
           src[i] = ent;
           ex[i] = __longlong_as_double(0x7ff8000000000000LL);
-          if (f < thr && !(p.debug & 2)) plist[atomicAdd((int*)&ctl[2], 1)] = i;
+          if (f < thr && (int64_t)ent.x > skp && !(p.debug & 2))
+            plist[atomicAdd((int*)&ctl[2], 1)] = i;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
         // exact scores of the entries under the published bound (debug bit 3:
-        // of every entry -- measured slower: the extra row reads outweigh
-        // warp 0's serial reads when the live bound rises past the published
-        // one).  Rows are read in batches of kXB per thread so their
-        // latencies overlap.
+        // of every entry).  Rows are read in batches of kXB per thread so
+        // their latencies overlap.
         const int nl = (p.debug & 8) ? len : ctl[2];
         constexpr int kXB = 6;
         for (int j0 = ptid; j0 < nl; j0 += kXB * kRP) {
@@ -1255,195 +1336,95 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         prep(0);
       }
       __syncthreads();
-      for (int ch = 0; ch < nc; ++ch) {
+      for (int ch = 0; ch < nc;) {
         const long long tw0 = clock64();
+        const bool rerun = ctl[14] != 0;  // (CTA-uniform: set before the last barrier)
+        const bool rescan = chunk[3 * ch + 2] >= 0;
         if (warp > 0) {
-          issue(ch + 3);
-          asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch+1 landed
-          asm volatile("bar.sync 1, %0;" ::"n"(kRP));
-          prep(ch + 1);
-        } else if (chunk[3 * ch + 2] < 0) {
+          if (!rerun) {
+            issue(ch + 3);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch+1 landed
+            asm volatile("bar.sync 1, %0;" ::"n"(kRP));
+            prep(ch + 1);
+          }
+        } else if (!rescan) {
           const uint4* src = ring + (ch % kRSlots) * kCH;
           const double* exs = ring_e + (ch % kRSlots) * kCH;
           const int len = chunk[3 * ch + 1];
+          const int64_t skp = (int64_t)*sskip;
           for (int w0 = 0; w0 < len; w0 += kWU * 32) {
             int32_t ids[kWU];
-            float fv[kWU];
             uint2 tl[kWU];
             double exv[kWU];
             bool valid[kWU];
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
               const int e = w0 + u * 32 + lane;
-              valid[u] = e < len;
-              const uint4 ent = valid[u] ? src[e] : make_uint4(0, 0, 0, 0);
+              const uint4 ent = e < len ? src[e] : make_uint4(0, 0, 0, 0);
+              valid[u] = e < len && (int64_t)ent.x > skp;  // walked items are decided
               ids[u] = (int32_t)ent.x;
-              fv[u] = -kInf;  // float64 fast score in .z/.w (prep) decides
-              tl[u] = make_uint2(ent.z, ent.w);
+              tl[u] = make_uint2(ent.z, ent.w);  // float64 fast score (prep)
               exv[u] = valid[u] ? exs[e] : 0.0;
             }
-            if (replay_window<16>(L, c, lane, ids, fv, tl, exv, valid, sid, sidx, sfv, sfe, lutf)) {
-              if (lane == 0) ctl[3] = 1;
+            const int b = replay_window<16>(L, c, lane, ids, tl, exv, valid, sid, sidx, sfv, sfe,
+                                            lutf, theta, -kInf64);
+            if (b >= 0) {  // the live threshold rose above theta: walk from the next item
+              const int32_t y = __shfl_sync(kFull, ids[b >> 5], b & 31);
+              if (lane == 0) { *walk_from = (long long)y + 1; ctl[3] = 1; }
               break;
             }
           }
           if (lane == 0) *pub_thr = L.thr64;
         }
-        if (chunk[3 * ch + 2] >= 0) {  // (CTA-uniform)
-          // candidates overflowed this slice's pages: rescan its items from the
-          // codes.  All four warps pre-filter a sub-range against T = the live
-          // bound + sigma (bit masks in this chunk's idle ring slot); warp 0
-          // decides the flagged items in order.  Unflagged items have fast >=
-          // T, so they stay unrefined until an insertion lifts the bound above
-          // T: the next sub-range then starts right after that insertion,
-          // pre-filtered against the new bound.
+        if (rescan) {  // (CTA-uniform)
+          // candidates overflowed this slice's pages: walk its items from the codes
           __syncthreads();
           const int64_t j = g0 + chunk[3 * ch + 2];
-          const int64_t lo = max(j * SW, st.P), hi_ = min((j + 1) * SW, n);
-          if (lo < hi_ && tid == 0) ++fallback_slices;
-          uint32_t* rmask = reinterpret_cast<uint32_t*>(ring + (ch % kRSlots) * kCH);  // 8 KiB
-          int32_t* rlst = reinterpret_cast<int32_t*>(ring_e + (ch % kRSlots) * kCH);  // 4 KiB
-          volatile double* tsub = reinterpret_cast<volatile double*>(ctl + 8);
-          constexpr int kSub = kCH * 16 * 8;  // items per sub-range: 2048 mask words (8 KiB)
-          auto fast_at = [&](int64_t i, uint2& tup) -> double {
-            const Row r2 = load_fast_row(p.codes_fast, FP, i);
-            double x;
-            if constexpr (FP <= 8) {
-              tup = make_uint2(r2.w[0], r2.w[1]);
-              x = tuple_f64<FP>(tup, lutf, m, F);
-            } else {
-              x = 0.0;  // float64 fast score in the reference's order
-#pragma unroll
-              for (int s2 = 0; s2 < FP; ++s2)
-                if (s2 < F) x = __dadd_rn(x, lutf[s2 * m + (int)r2.byte(s2)]);
-              const unsigned long long db = (unsigned long long)__double_as_longlong(x);
-              tup = make_uint2((uint32_t)db, (uint32_t)(db >> 32));
-            }
-            return x;
-          };
-          // one decision window over items given by position -> id
-          auto walk = [&](auto id_at, int npos, int p0, double cap, int* brk) -> bool {
-            for (int w0 = p0; w0 < npos; w0 += kWU * 32) {
-              int32_t ids2[kWU];
-              float f2[kWU];
-              uint2 t2[kWU];
-              double e2[kWU];
-              bool valid2[kWU];
-#pragma unroll
-              for (int u = 0; u < kWU; ++u) {
-                const int x = w0 + u * 32 + lane;
-                valid2[u] = x < npos;
-                const int64_t i = valid2[u] ? id_at(x) : 0;
-                ids2[u] = (int32_t)i;
-                f2[u] = -kInf;  // no float32 score: the exact float64 one decides
-                t2[u] = make_uint2(0u, 0u);
-                e2[u] = __longlong_as_double(0x7ff8000000000000LL);
-                if (valid2[u]) (void)fast_at(i, t2[u]);
-              }
-              int b = -1;
-              if (replay_window<FP>(L, c, lane, ids2, f2, t2, e2, valid2, sid, sidx, sfv, sfe, lutf,
-                                    cap, brk ? &b : nullptr))
-                return true;
-              if (b >= 0) { *brk = w0 + b; return false; }
-            }
-            return false;
-          };
-          bool stopped = false;
-          volatile long long* snext = reinterpret_cast<volatile long long*>(ctl + 10);
-          if constexpr (FP > 2) {
-            // wider fast codes (c3/c4 shapes) rarely overflow: warp 0 walks the
-            // slice alone and the kernel keeps its smaller register footprint
-            if (warp == 0) {
-              stopped = walk([&](int x) { return lo + x; }, (int)max((int64_t)0, hi_ - lo), 0,
-                             kInf64, nullptr);
-              if (lane == 0 && stopped) ctl[3] = 1;
+          const int64_t lo = max(max(j * SW, st.P), (int64_t)*sskip + 1), hi_ = min((j + 1) * SW, n);
+          if (lo < hi_) {
+            if (tid == 0) ++fallback_slices;
+            // (a rescan chunk is never staged: its ring slot (8 KiB of mask
+            // words, 64k-item sub-ranges) and exact-score slot are free)
+            walk(lo, hi_, false, reinterpret_cast<uint32_t*>(ring + (ch % kRSlots) * kCH),
+                 reinterpret_cast<int32_t*>(ring_e + (ch % kRSlots) * kCH), kCH * 16 * 8);
+            if (warp == 0 && lane == 0 && L.thr64 > theta && hi_ < n) {
+              *walk_from = hi_;  // the lists stop covering the items after the slice
+              ctl[3] = 1;
             }
           }
-          for (int64_t s0 = lo; FP <= 2 && s0 < hi_ && !stopped;) {
-            const int64_t s1 = min(hi_, s0 + (int64_t)kSub);
-            const int nsub = (int)(s1 - s0);
-            if (warp == 0 && lane == 0) *tsub = (p.debug & 16) ? -kInf64 : L.thr64;
-            __syncthreads();
-            const double T = *tsub;
-            constexpr int kPW = 16;
-            // kPW words per warp and pass: the row reads of a pass overlap
-            for (int b0 = warp * 32 * kPW; b0 < nsub; b0 += kRW * 32 * kPW) {
-              Row rows[kPW];
-#pragma unroll
-              for (int u = 0; u < kPW; ++u) {
-                const int x = b0 + u * 32 + lane;
-                if (x < nsub) rows[u] = load_fast_row(p.codes_fast, FP, s0 + x);
-              }
-#pragma unroll
-              for (int u = 0; u < kPW; ++u) {
-                const int x = b0 + u * 32 + lane;
-                bool under = false;
-                if (x < nsub) {
-                  double f = 0.0;  // float64 fast score in the reference's order
-#pragma unroll
-                  for (int s2 = 0; s2 < FP; ++s2)
-                    if (s2 < F) f = __dadd_rn(f, lutf[s2 * m + (int)rows[u].byte(s2)]);
-                  under = f < T;
-                }
-                const uint32_t bw = __ballot_sync(kFull, under);
-                if (lane == 0 && b0 + u * 32 < nsub) rmask[(b0 >> 5) + u] = bw;
-              }
-            }
-            __syncthreads();
-            if (warp == 0) {
-              int from = 0;  // sub-range position where the one-by-one walk starts
-              int64_t next = s1;
-              if (L.thr64 <= T) {
-                from = nsub;
-                const int nwords = (nsub + 31) >> 5;
-                for (int w0 = 0; w0 < nwords && !stopped; w0 += 32) {
-                  const uint32_t wv = w0 + lane < nwords ? rmask[w0 + lane] : 0u;
-                  const int cw = __popc(wv);
-                  int incl = cw;
-#pragma unroll
-                  for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
-                  }
-                  const int nl = __shfl_sync(kFull, incl, 31);
-                  int o = incl - cw;
-                  for (uint32_t bb = wv; bb; bb &= bb - 1) rlst[o++] = (w0 + lane) * 32 + __ffs(bb) - 1;
-                  __syncwarp();
-                  int brk = -1;
-                  stopped = walk([&](int x) { return s0 + rlst[x]; }, nl, 0, T, &brk);
-                  __syncwarp();
-                  if (brk >= 0) { next = s0 + rlst[brk] + 1; break; }  // bound rose above T
-                }
-              }
-              if (!stopped && from < nsub)
-                stopped = walk([&](int x) { return s0 + x; }, nsub, from, kInf64, nullptr);
-              if (lane == 0) {
-                if (stopped) ctl[3] = 1;
-                *snext = (long long)next;
-              }
-            }
-            __syncthreads();
-            stopped = ctl[3] != 0;
-            s0 = (int64_t)*snext;
-          }
-          if (warp == 0 && lane == 0) *pub_thr = L.thr64;
         }
         const long long tw1 = clock64();
         __syncthreads();
         if (warp == 0) { t_work += tw1 - tw0; t_wait += clock64() - tw1; }
-        if (ctl[3]) break;  // insertion budget spent: the next round resumes at *stop_pos
+        if (ctl[3]) {  // (CTA-uniform) walk until the threshold is back under theta
+          const int64_t from = (int64_t)*walk_from;
+          __syncthreads();
+          if (tid == 0) ctl[3] = 0;
+          // scratch: the exact-score slots of chunks ch+2 and ch+3 (their
+          // entries may still be landing, but prep fills those slots only in
+          // the iterations ch+1 / ch+2); 4 KiB each -> 32k-item sub-ranges
+          walk(from, n, true, reinterpret_cast<uint32_t*>(ring_e + ((ch + 2) % kRSlots) * kCH),
+               reinterpret_cast<int32_t*>(ring_e + ((ch + 3) % kRSlots) * kCH), kCH * 8 * 8);
+          if (tid == 0) ctl[14] = 1;  // decide the rest of chunk ch (ids after the walk)
+          __syncthreads();
+        } else {
+          if (tid == 0) ctl[14] = 0;
+          __syncthreads();
+          ++ch;
+        }
+        if (*sskip >= n - 1 || ctl[13]) break;  // (CTA-uniform) walked to the end / stopped
       }
       if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+      if (tid == 0) ctl[14] = 0;
       __syncthreads();
-      if (ctl[3]) break;
     }
     if (warp == 0) L.H.store(lane);
   }
   __syncthreads();
-  if (ctl[3]) {
-    // budget spent: hand the state to the next round (heap sorted descending,
-    // resume position, a fresh threshold with 4x the budget, unbudgeted M in
-    // the last round)
+  if (ctl[13]) {
+    // a walk ran past p.walk_cap: hand the query to the next round -- the
+    // heap (sorted descending), the first undecided item and, as the new
+    // list threshold, the live threshold itself (J = 0)
     for (int i = tid; i < k; i += kRW * 32) {
       p.heap_e[(size_t)q * k + i] = he[i];
       p.heap_f[(size_t)q * k + i] = hf[i];
@@ -1451,36 +1432,21 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
     }
     if (tid == 0) {
       QState ns = st;
-      ns.P = *stop_pos;
+      ns.P = (int64_t)*sskip + 1;
       ns.refinements = L.refinements;
       ns.insertions = L.insertions;
-      ns.ins0 = L.insertions;
-      // next budget: as many insertions as A_j stays near the live bound
-      // (recomputed from the heap; the last round is unbudgeted)
-      int J = (p.round + 2 >= p.max_rounds || st.J >= kInfBudget) ? kInfBudget : kSelectJ;
-      if (J >= k - 1) J = kInfBudget;
-      const int top = J == kInfBudget ? k : J + 1;
-      int best = 0;
-      for (int i = 1; i < top; ++i) {
-        if (J != kInfBudget && p.j0 < 0 && hf[i] > hf[0] * (1.0 + p.budget_slack)) {
-          J = i - 1;  // stay near the live bound: grow the budget only while A_j does
-          break;
-        }
-        if (hf[i] > hf[best]) best = i;
-      }
-      ns.J = J;
-      ns.thr = hf[best];
+      ns.thr = L.thr64;
       certified_bounds(ns.thr, F, ns.lo, ns.hi);
-      if (st.mt_valid) {
-        const Row r = load_fast_row(p.codes_fast, FP, hi[best]);
+      if (st.mt_valid) {  // sigma == 0: the heap maximum's tuple ties at thr exactly
+        const Row r = load_fast_row(p.codes_fast, FP, hi[0]);
         ns.mtup[0] = r.w[0];
         ns.mtup[1] = r.w[1];
       }
-      ns.rounds = st.rounds + 1;
       ns.ovf_pages = 0;
       ns.ovf_pool = 0;
+      ns.rounds = st.rounds + 1;
+      ns.walked = st.walked + walked;
       p.qs[q] = ns;
-      atomicAdd(&p.active[p.round], 1);
     }
     return;
   }
@@ -1500,12 +1466,12 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       int64_t* s = p.stats + (size_t)q * kStats;
       s[0] = L.insertions;
       s[1] = L.candidates;
-      s[2] = st.rounds + 1;  // filter/replay rounds this query used
+      s[2] = st.walked + walked;
       s[3] = st.P;
       s[4] = st.pro_cycles;
       s[5] = clock64() - t0;
       s[6] = fallback_slices | ((int64_t)p.qs[q].ovf_pages << 20) | ((int64_t)p.qs[q].ovf_pool << 40);
-      s[7] = st.wide;
+      s[7] = st.wide | ((int64_t)(st.rounds + 1) << 8);  // wide flag | rounds used << 8
       s[8] = st.pro_cand;
       s[9] = listed;
       s[10] = st.insertions;
@@ -1524,27 +1490,39 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
 template <int FP>
 cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cudaEvent_t* ev) {
   using G = FGeo<FP>;
+  // kernel attributes once per process (they are per function, not per launch)
+  static cudaError_t attr[64];
+  static std::once_flag once[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [&] {
+    attr[dev] = [&] {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(icq_prologue_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kSmemWindow - kDynBase))) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(icq_filter_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kSmemWindow - kDynBase))) != cudaSuccess)
+      return e;
+    return cudaFuncSetAttribute(icq_replay_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kSmemWindow - kDynBase));
+    }();
+  });
+  if (attr[dev] != cudaSuccess) return attr[dev];
   const ProLayout pl = pro_layout(p.K, p.m, p.F, p.k);
   const RepLayout rl = rep_layout(p.K, p.m, p.F, p.k);
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(icq_prologue_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pl.total)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(icq_filter_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(kSmemWindow - kDynBase))) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(icq_replay_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)rl.total)) != cudaSuccess)
-    return e;
   if (ev) cudaEventRecord(ev[0], s);
   icq_prologue_kernel<FP><<<p.Q, kProThreads, pl.total, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (ev) cudaEventRecord(ev[1], s);
-  // filter / replay rounds: a query whose insertion budget ran out resumes
-  // in the next round; finished queries cost the later launches nothing
-  for (int r = 0; r < p.max_rounds; ++r) {
+  // filter / replay rounds: a query whose walk ran too long resumes in the
+  // next round; finished queries cost the later launches nothing
+  for (int r = 0; r < p.rounds; ++r) {
     PipeParams pr = p;
     pr.round = r;
+    pr.last_round = r + 1 == p.rounds ? 1 : 0;
     if (r > 0 && (e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
     icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1553,7 +1531,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3 + 2 * r], s);
   }
-  for (int r = p.max_rounds; ev && r < kRounds; ++r) {  // unused rounds: empty intervals
+  for (int r = p.rounds; ev && r < kMaxRounds; ++r) {  // unused rounds: empty intervals
     cudaEventRecord(ev[2 + 2 * r], s);
     cudaEventRecord(ev[3 + 2 * r], s);
   }

@@ -28,20 +28,18 @@ struct QState {
   int64_t pro_t[4];     // prologue phase cycles: prefilter, scoring, decisions, blocks
   int32_t ovf_pages;    // filter slices over kMaxPages (diagnostics)
   int32_t ovf_pool;     // filter slices that found the pool exhausted
-  double thr;           // filter threshold: candidate iff fast64 < thr
+  double thr;           // list threshold theta: the lists hold every item with fast64 < thr
   uint32_t mtup[2];     // fast-code bytes of the heap item whose fast score is thr
   int32_t mt_valid;     // (sigma == 0: items with this tuple tie at thr exactly)
   float lo, hi;         // its certified float32 bounds (x32 < lo: yes, x32 >= hi: no)
   int32_t wide;         // float32 certification off: float64 only
-  int32_t J;            // insertion budget of thr (kInfBudget: always valid)
-  int64_t ins0;         // insertions when thr was set
-  int32_t done;         // all items decided, outputs written
-  int32_t rounds;       // filter/replay rounds used
+  int32_t done;         // all items decided, outputs written (later rounds skip it)
+  int32_t rounds;       // filter/replay rounds before this one
+  int32_t pad_;
+  int64_t walked;       // items walked in order in earlier rounds
   int64_t skipped;      // items the filter did not stream (their slice overflowed:
                         // the replay rescans it from the codes)
 };
-constexpr int32_t kInfBudget = 1 << 30;
-constexpr int kRounds = 8;  // filter/replay rounds (the last one filters with M: no budget)
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries; the filter indexes by gg >> 7)
@@ -49,7 +47,9 @@ constexpr int kMaxPages = 64;    // pages per slice (more -> the replay rescans 
 constexpr int kSliceInts = 4 + kMaxPages;  // count, 3 pad, page ids (16-byte rows)
 constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
-constexpr int64_t kRangeAlign = 32768;  // ranges / padding: whole filter tiles of every warp
+constexpr int64_t kRangeAlign = 32768;
+constexpr int kMaxRounds = 4;  // filter/replay rounds per batch (walks past walk_cap resume)
+constexpr int kProfEvents = 2 + 2 * kMaxRounds;  // ranges / padding: whole filter tiles of every warp
 
 struct PipeParams {
   const uint8_t* codes_fast;  // [n_pad * FP]   fast books only (row-major), zero padded
@@ -69,7 +69,6 @@ struct PipeParams {
   uint4* pool;                // [pool_pages * kPG] candidates {id, 0, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
-  int32_t* active;            // [kRounds] queries handed to round r+1 by the replay of round r
   int64_t pool_pages;
   int64_t n;
   int64_t words;              // survivors bitmap words per query
@@ -82,20 +81,23 @@ struct PipeParams {
   int32_t pro_div;            // prologue stops once a block's candidates <= items / pro_div
   int32_t debug;              // experiments only (ICQ_DEBUG): bit 0 = no tuple-tie rejection,
                               // bit 1 = replay producers skip exact scores
-  int32_t round;              // current filter/replay round (0-based)
-  int32_t j0;                 // first-round insertion budget (-1: from the insertion rate)
-  int32_t max_rounds;         // filter/replay rounds (1: no insertion budgets, threshold M)
-  double budget_slack;        // A_J may exceed the live bound A_0 by this relative margin
+  int32_t list_j;             // list threshold theta = A_J + sigma at the prologue end (A_J:
+                              // max fast score over the J+1 largest-exact heap entries)
+  int32_t pro_live;           // prologue stop rule counts items under theta (1) or under M (0)
+  int32_t sigma_f32;          // numpy promotion of a float32 sigma (see live_thr)
+  int32_t rounds;             // filter/replay rounds (1..kMaxRounds)
+  int32_t round, last_round;  // this launch's round
+  int64_t walk_cap;           // an in-order walk longer than this hands the query to the next round
   int64_t pro_min, pro_max;   // prologue length bounds (items)
   uint8_t fast_books[kMaxK];
 };
 
 bool make_lut_prog(int d, LutProg* out);
 cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, int m, int d,
-                       int Q, const LutProg* prog_dev, cudaStream_t s);
+                       int Q, const LutProg* prog_dev, int32_t* err, cudaStream_t s);
 // prologue -> filter -> replay for one batch (icq_pipeline.cu)
-// ev: optional 2 + 2 * kRounds events: before/after the prologue, then after the
-// filter and after the replay of every round
+// ev: optional kProfEvents events: before the prologue, after the prologue,
+// then after the filter and the replay of every round
 cudaError_t launch_pipeline(const PipeParams& p, int FP, int filter_ctas, cudaStream_t s,
                             int* unsupported, cudaEvent_t* ev = nullptr);
 

@@ -14,8 +14,44 @@ from dataclasses import dataclass, field
 import numpy as np
 
 
-class ValidationError(ValueError):
+def _reference_classes():
+    """The reference's exception classes when its package is importable.
+
+    A drop-in must raise the *same* classes the reference's callers catch
+    (``except icq.ValidationError``, ``pytest.raises(ValidationError)`` in
+    pkg/tests/test_search.py:126-141, :218-221).  When ``icq`` is importable
+    the mirror's classes derive from the reference's, so both the local and
+    the reference class match; without it they are plain ValueError /
+    Exception subclasses with the reference's names and meanings.
+    ``ICQ_B200_STANDALONE=1`` skips the probe.
+    """
+    import importlib.util
+    import os
+
+    if os.environ.get("ICQ_B200_STANDALONE"):
+        return ValueError, Exception, Exception
+    try:
+        if importlib.util.find_spec("icq") is None:
+            return ValueError, Exception, Exception
+        import icq.data as ref
+    except Exception:  # pragma: no cover - a broken reference install
+        return ValueError, Exception, Exception
+    return ref.ValidationError, ref.FormatError, ref.UnsupportedVersionError
+
+
+_VE_BASE, _FE_BASE, _UVE_BASE = _reference_classes()
+
+
+class ValidationError(_VE_BASE):  # type: ignore[misc,valid-type]
     """Invalid values: non-finite data, bad shapes, out-of-range parameters (data.py:32)."""
+
+
+class FormatError(_FE_BASE):  # type: ignore[misc,valid-type]
+    """Malformed file: bad magic, truncated payload, inconsistent lengths (data.py:36)."""
+
+
+class UnsupportedVersionError(FormatError, _UVE_BASE):  # type: ignore[misc,valid-type]
+    """Index file written with an unknown format version (data.py:40)."""
 
 
 class UnsupportedError(RuntimeError):

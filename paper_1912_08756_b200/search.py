@@ -30,8 +30,8 @@ from .data import DeviceError, UnsupportedError, ValidationError
 
 # per-query int64 diagnostics written by the replay kernel (icq_b200.h stats_dev)
 STATS_FIELDS = 16
-STATS_NAMES = ("insertions", "replay_candidates", "filter_rounds", "prologue_end",
-               "prologue_cycles", "replay_cycles", "rescanned_slices", "wide",
+STATS_NAMES = ("insertions", "replay_candidates", "walked_items", "prologue_end",
+               "prologue_cycles", "replay_cycles", "rescanned_slices", "wide_rounds",
                "prologue_f64_scored", "filter_candidates", "prologue_insertions",
                "filter_hi_f32_bits", "prologue_filter_cycles", "prologue_score_cycles",
                "prologue_decide_cycles", "filter_skipped_items")
@@ -71,6 +71,29 @@ class BatchResult:
     refinements: np.ndarray
     ops: list
     fallback: bool = False
+
+
+FLAG_EXACT = 1       # icq_b200.h ICQ_FLAG_EXACT
+FLAG_SIGMA_F32 = 2   # icq_b200.h ICQ_FLAG_SIGMA_F32
+
+
+def _sigma_flags(sigma) -> tuple[float, int]:
+    """sigma as the float64 the C ABI takes, plus the promotion flag.
+
+    The reference computes ``bound + sigma`` (search.py:149) with whatever
+    scalar type the caller passed.  A numpy float32 sigma makes numpy 2
+    evaluate that sum -- and the comparison -- in float32 once the heap
+    maximum is an inserted entry (NEP 50); ICQ_FLAG_SIGMA_F32 reproduces it
+    on the device.  Python floats, ints and float64 stay float64; other
+    reduced/extended numpy float types are rejected rather than silently
+    computed differently.
+    """
+    if isinstance(sigma, np.floating) and not isinstance(sigma, np.float64):
+        if isinstance(sigma, np.float32):
+            return float(sigma), FLAG_SIGMA_F32
+        raise UnsupportedError(f"sigma of type {type(sigma).__name__} is not supported "
+                               "(use a Python float, np.float64 or np.float32)")
+    return float(sigma), 0
 
 
 def _raise(code: int, what: str):
@@ -178,7 +201,7 @@ class DeviceIndex:
         return self._h
 
     def search_lut_device(self, lut, k: int, sigma: float = 0.0, exact: bool = False, out=None,
-                          stats=False, stream=None):
+                          stats=False, stream=None, survivors=False):
         """Search on a precomputed device float64 LUT (nq, K, m); torch outputs."""
         import torch
 
@@ -190,27 +213,36 @@ class DeviceIndex:
                 "scores": torch.empty((nq, k), dtype=torch.float64, device=dev),
                 "refinements": torch.empty((nq,), dtype=torch.int64, device=dev),
             }
+            if survivors:
+                out["survivors"] = torch.empty((nq, (self.n + 31) // 32), dtype=torch.int32,
+                                               device=dev)
             if stats:
                 out["stats"] = torch.empty((nq, STATS_FIELDS), dtype=torch.int64, device=dev)
         s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
         fb = C.c_int32(0)
+        sig, flags = _sigma_flags(sigma)
         st = _native.lib().icq_search_with_lut(
-            self._h, lut.data_ptr(), nq, k, float(sigma), int(exact), out["ids"].data_ptr(),
-            out["scores"].data_ptr(), out["refinements"].data_ptr(), None,
+            self._h, lut.data_ptr(), nq, k, sig, flags | (FLAG_EXACT if exact else 0),
+            out["ids"].data_ptr(),
+            out["scores"].data_ptr(), out["refinements"].data_ptr(),
+            out["survivors"].data_ptr() if "survivors" in out else None,
             out["stats"].data_ptr() if "stats" in out else None, C.byref(fb), s)
         if st != _native.ICQ_OK:
             _raise(st, "icq_search_with_lut")
+        out["fallback"] = bool(fb.value)
         return out
 
     # -- host-buffer path (used by the reference-shaped API) ------------------
-    def search_host(self, Q: np.ndarray, k: int, sigma: float, exact: bool):
+    def search_host(self, Q: np.ndarray, k: int, sigma, exact: bool):
         Q = np.ascontiguousarray(Q, dtype=np.float64)
         nq = Q.shape[0]
         ids = np.empty((nq, k), dtype=np.int64)
         scores = np.empty((nq, k), dtype=np.float64)
         refine = np.empty((nq,), dtype=np.int64)
         fb = C.c_int32(0)
-        st = _native.lib().icq_search_host(self._h, Q.ctypes.data, nq, k, float(sigma), int(exact),
+        sig, flags = _sigma_flags(sigma)
+        st = _native.lib().icq_search_host(self._h, Q.ctypes.data, nq, k, sig,
+                                           flags | (FLAG_EXACT if exact else 0),
                                            ids.ctypes.data, scores.ctypes.data,
                                            refine.ctypes.data, C.byref(fb))
         if st != _native.ICQ_OK:
@@ -236,6 +268,10 @@ class DeviceIndex:
 
         if q.dtype != torch.float64 or q.dim() != 2 or q.shape[1] != self.d or not q.is_cuda:
             raise ValidationError("q must be a cuda float64 tensor of shape (nq, d)")
+        if not exact and _sigma_flags(sigma)[1]:  # float32 sigma: the flags entry point
+            lut = self.build_lut_device(q, stream=stream)
+            return self.search_lut_device(lut, k, sigma, out=out, stats=stats, stream=stream,
+                                          survivors=survivors)
         q = q.contiguous()
         nq = q.shape[0]
         dev = q.device
@@ -269,6 +305,8 @@ class DeviceIndex:
                 workspace.data_ptr(), workspace.numel(), s)
         if st != _native.ICQ_OK:
             _raise(st, "icq_search")
+        if exact:  # search_exact refines every element (search.py:108)
+            out["refinements"].fill_(self.n)
         out["fallback"] = bool(fb.value)
         return out
 
@@ -381,7 +419,7 @@ def search_two_step(index, q, k: int, sigma: float | None = None) -> QueryResult
         res.fallback = True
         return res
     q = _check_query(q, index.d)
-    ids, scores, refine, _ = device_index(index).search_host(q[None], k, float(sigma), exact=False)
+    ids, scores, refine, _ = device_index(index).search_host(q[None], k, sigma, exact=False)
     R = int(refine[0])
     return QueryResult(ids=ids[0], scores=scores[0], ops=_ops_two_step(index, R, k))
 
@@ -395,7 +433,7 @@ def search_two_step_batch(index, queries, k: int, sigma: float | None = None) ->
         raise ValidationError(f"sigma must be >= 0, got {sigma}")
     Q = _check_queries(queries, index.d)
     exact = np.asarray(index.fast).size == 0
-    ids, scores, refine, fb = device_index(index).search_host(Q, k, float(sigma), exact=exact)
+    ids, scores, refine, fb = device_index(index).search_host(Q, k, sigma, exact=exact)
     if exact:
         ops = [_ops_exact(index) for _ in range(Q.shape[0])]
         refine = np.full(Q.shape[0], index.n, dtype=np.int64)

@@ -14,6 +14,9 @@ class Row:
         self.k = int(r[1])
         self.sigma = None if r[2] == -1.0 else float(r[2])
         self.is_exact = bool(r[3])
+        self.sigma_f32 = len(r) > 4 and bool(r[4])
+        if self.sigma_f32:  # the reference was called with a numpy float32 sigma
+            self.sigma = np.float32(self.sigma)
         self.ids = z[f"r{i}_ids"]
         self.scores = z[f"r{i}_scores"]
         ops = z[f"r{i}_ops"]

@@ -79,32 +79,42 @@ CONFIGS = [
 
 # Pipeline shapes (icq_capi.cu planning knobs, read on every call):
 #   default   - the prologue decides small databases alone
-#   filter    - 2048-item prologue: the filter kernel + in-order replay of its slices
+#   filter    - 2048-item prologue: the filter kernel lists every item under
+#               theta = the live threshold at the prologue end; the replay
+#               decides the lists and walks the database in order whenever
+#               the live threshold rises above theta
+#   listj     - as filter, theta = A_5 + sigma (max fast over the 6 largest
+#               heap entries): longer lists, fewer walks
+#   prolive   - as filter with a 16k-item cap, the prologue stop rule counts
+#               items under theta instead of the stale M
 #   overflow  - as filter, with a 2-page candidate pool: slices overflow and
-#               the replay rescans them from the codes
+#               the replay walks them from the codes
 #   subbatch  - as filter, queries in sub-batches of 4
-#   rounds    - as filter, insertion budget 1: several filter/replay rounds
-#   rounds3   - budget 0 and 3 rounds: the last round filters with M
+#   rangemajor- as filter, range-major unit order over 32k-item ranges
 #   noprep    - as filter, the replay's preparing warps score nothing exactly:
 #               warp 0 reads every refined row itself (ICQ_DEBUG bit 1)
 #   allexact  - as filter, the preparing warps score every entry (bit 3)
 #   noties    - as filter, no tuple-tie rejection in the filter (bit 0)
-#   overflow_walk - as overflow, rescans walked item by item by warp 0 (bit 4)
+#   overflow_walk - as overflow, walks flag every item (bit 4)
+#   rounds    - as filter, every walk past 1 item stops the query; the next
+#               filter/replay round lists its rest (4 rounds, the last unbounded)
+#   oneround  - as filter, a single round (walks run to completion)
+_F = {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"}
 MODES = {
     "default": {},
-    "filter": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"},
-    "overflow": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_POOL_PAGES": "2"},
+    "filter": dict(_F),
+    "listj": dict(_F, ICQ_LIST_J="5"),
+    "prolive": {"ICQ_PRO_MAX": "16384", "ICQ_PRO_MIN": "0", "ICQ_PRO_LIVE": "1"},
+    "overflow": dict(_F, ICQ_POOL_PAGES="2"),
     "subbatch": {"ICQ_PRO_MAX": "4096", "ICQ_PRO_MIN": "0", "ICQ_QBATCH": "4"},
-    # insertion budget 1: the replay stops after two insertions and the next
-    # round re-filters the rest (the third round filters with M, unbudgeted)
-    "rounds": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "1", "ICQ_ROUNDS": "8"},
-    "rounds3": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_J0": "0", "ICQ_ROUNDS": "3"},
-    "noprep": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "2"},
-    "allexact": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "8"},
-    "noties": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_DEBUG": "1"},
-    # overflow rescans without the cooperative pre-filter (warp 0 walks all)
-    "overflow_walk": {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0", "ICQ_POOL_PAGES": "2",
-                      "ICQ_DEBUG": "16"},
+    "rangemajor": dict(_F, ICQ_RANGE_MAJOR="1", ICQ_RANGE_ITEMS="32768"),
+    "noprep": dict(_F, ICQ_DEBUG="2"),
+    "allexact": dict(_F, ICQ_DEBUG="8"),
+    "noties": dict(_F, ICQ_DEBUG="1"),
+    "overflow_walk": dict(_F, ICQ_POOL_PAGES="2", ICQ_DEBUG="16"),
+    # walks longer than 1 item hand the query to the next filter/replay round
+    "rounds": dict(_F, ICQ_WALK_CAP="1", ICQ_ROUNDS="4"),
+    "oneround": dict(_F, ICQ_ROUNDS="1"),
 }
 
 
@@ -120,7 +130,7 @@ def test_random_vs_oracle_with_survivors(cfg, mode, monkeypatch):
     Q = rng.standard_normal((6, d))
     qd = torch.from_numpy(Q).cuda()
     for k in (1, 10, 100):
-        for sigma in (0.0, 1.0, 25.0, 1e18):
+        for sigma in (0.0, 1.0, 25.0, 1e18, np.float32(2.5)):
             out = dev.search_device(qd, k, sigma, survivors=True, stats=True)
             torch.cuda.synchronize()
             ids = out["ids"].cpu().numpy()
@@ -208,6 +218,20 @@ def test_validation_errors():
         icqb.DeviceIndex(books, bad, fast)
     with pytest.raises(icqb.ValidationError):
         icqb.DeviceIndex(books, codes, np.array([1, 0], dtype=np.uint32))
+    # non-finite queries: rejected on the host path, and by the LUT kernel's
+    # device check on the device-pointer entry points (search.py:51-52)
+    bad_q = q.copy()
+    bad_q[0, 2] = np.nan
+    with pytest.raises(icqb.ValidationError):
+        dev.search_host(bad_q, 3, 0.0, exact=False)
+    with pytest.raises(icqb.ValidationError):
+        dev.search_device(torch.from_numpy(bad_q).cuda(), 3, 0.0)
+    with pytest.raises(icqb.ValidationError):
+        dev.build_lut_device(torch.from_numpy(np.full((2, 4), np.inf)).cuda())
+    # a later clean call is unaffected (the error word is per call)
+    dev.search_device(torch.from_numpy(q).cuda(), 3, 0.0)
+    with pytest.raises(icqb.UnsupportedError):
+        dev.search_host(q, 3, np.float16(1.0), exact=False)
     with pytest.raises(icqb.UnsupportedError):
         icqb.DeviceIndex(rng.standard_normal((2, 300, 4)).astype(np.float32),
                          rng.integers(0, 300, size=(10, 2)).astype(np.uint32),
