@@ -406,18 +406,20 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   }
   p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 512);
   p.debug = (int32_t)env_i("ICQ_DEBUG", 0);  // experiments only; results stay exact
-  // list threshold theta = A_J + sigma: J = 0 is the live threshold at the
-  // prologue end (sigma == 0: anything looser lists millions of items on c5);
-  // with sigma > 0 the margin dominates the lists and a deeper J spares walks
-  p.list_j = (int32_t)env_i("ICQ_LIST_J", p.sigma == 0.0 ? 0 : 32);
+  // list threshold theta = A_J + sigma (J = 0: the live threshold at the
+  // prologue end; deeper J: looser lists, fewer in-order walks); by default
+  // the prologue picks the loosest J whose list share stays <= 1/list_div
+  p.list_j = (int32_t)env_i("ICQ_LIST_J", -1);
+  p.list_div = (int32_t)env_i("ICQ_LIST_DIV", 128);
   p.pro_live = (int32_t)env_i("ICQ_PRO_LIVE", 0);
   {
-    const int64_t r = env_i("ICQ_ROUNDS", 3);
+    const int64_t r = env_i("ICQ_ROUNDS", kMaxRounds);
     p.rounds = (int32_t)(r < 1 ? 1 : (r > kMaxRounds ? kMaxRounds : r));
     // one replay CTA walks ~1 item per clock; a filter round lists a query's
-    // rest on every SM: hand walks longer than ~n/64 (>= 1M items) over
-    int64_t wc = h->n / 64;
-    p.walk_cap = env_i("ICQ_WALK_CAP", wc < ((int64_t)1 << 20) ? ((int64_t)1 << 20) : wc);
+    // rest on every SM in microseconds: hand over after max(128k, n/512) items
+    int64_t wc = h->n / 512;
+    if (wc < ((int64_t)1 << 17)) wc = (int64_t)1 << 17;
+    p.walk_cap = env_i("ICQ_WALK_CAP", wc);
   }
   p.pro_min = env_i("ICQ_PRO_MIN", 8192);
   {

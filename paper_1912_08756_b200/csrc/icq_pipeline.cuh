@@ -150,7 +150,7 @@ __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   L.ring = o;  o = al16(o + kRSlots * kCH * 16);
   L.ringe = o; o = al16(o + kRSlots * kCH * 8);
   L.plist = o; o = al16(o + kCH * 4);
-  L.ctl = o;   o = al16(o + 64);
+  L.ctl = o;   o = al16(o + 128);
   L.total = o;
   return L;
 }
@@ -492,9 +492,74 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   //    The filter lists every later item with fast < theta; the replay walks
   //    the database in order wherever the live threshold rises above theta.
   __syncthreads();
+  // 4a. the list threshold: theta_J = A_J + sigma for J on a ladder; the
+  //     loosest one whose share of the last <= 16k prologue items stays
+  //     <= 1/list_div (the items after P come from the same stream).  Loose
+  //     lists cost list entries (cheap, filtered on every SM), tight ones
+  //     cost walks whenever the live threshold rises above theta (in order,
+  //     one CTA).  ICQ_LIST_J >= 0 fixes J.
+  int listJ = p.list_j;
+  if (listJ < 0) {
+    constexpr int kLad = 9;
+    const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30};
+    float* lad_hi = reinterpret_cast<float*>(cf);        // (cf/ce are free now)
+    int* lad_cnt = reinterpret_cast<int*>(cf + 16);
+    if (warp == 0) {
+      for (int r = 0; r < kLad; ++r) {
+        const double A = heap_AJ(hf, k, min(ladder[r], k - 1), lane, nullptr);
+        float lo_ = kInf, hi_ = kInf;
+        certified_bounds(thr_cover(A, p.sigma, f32s, false), F, lo_, hi_);
+        if (lane == 0) { lad_hi[r] = hi_; lad_cnt[r] = 0; }
+      }
+    }
+    __syncthreads();
+    int64_t S = (pos - k) / kProBlock * kProBlock;
+    if (S > 8 * kProBlock) S = 8 * kProBlock;
+    if (wide || pos >= n) S = 0;
+    int cnt[kLad];
+#pragma unroll
+    for (int r = 0; r < kLad; ++r) cnt[r] = 0;
+    for (int64_t i0 = pos - S + (int64_t)tid * 8; i0 < pos; i0 += kProThreads * 8) {
+      uint32_t w[2 * FP];
+      if (FP == 1) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p.codes_fast + perm_offset(1, i0)));
+        w[0] = v.x; w[1] = v.y;
+      } else {
+        constexpr int kIpc = 16 / (FP > 1 ? FP : 1);
+#pragma unroll
+        for (int t = 0; t < FP / 2; ++t) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(p.codes_fast) + perm_chunk(i0 / kIpc + t));
+          w[4 * t] = v.x; w[4 * t + 1] = v.y; w[4 * t + 2] = v.z; w[4 * t + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float x = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < FP; ++s2) {
+          const int b = j * FP + s2;
+          const uint32_t code = (w[b >> 2] >> ((b & 3) * 8)) & 0xffu;
+          if (s2 < F) x += lut32[s2 * m + code];
+        }
+#pragma unroll
+        for (int r = 0; r < kLad; ++r) cnt[r] += x < lad_hi[r] ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kLad; ++r) {
+      const int c2 = __reduce_add_sync(kFull, cnt[r]);
+      if (lane == 0 && c2) atomicAdd(&lad_cnt[r], c2);
+    }
+    __syncthreads();
+    listJ = 0;
+    for (int r = 0; r < kLad; ++r)
+      if (S > 0 && (int64_t)lad_cnt[r] * p.list_div <= S) listJ = ladder[r];
+    listJ = min(listJ, k - 1);
+    __syncthreads();
+  }
   if (warp == 0) {
     int best = 0;
-    const double A = heap_AJ(hf, k, p.list_j, lane, &best);
+    const double A = heap_AJ(hf, k, listJ, lane, &best);
     double thr = wide ? kInf64 : thr_cover(A, p.sigma, f32s, false);
     float flo = kInf, fhi = kInf;
     if (!wide) certified_bounds(thr, F, flo, fhi);
@@ -1007,8 +1072,9 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   double* ring_e = reinterpret_cast<double*>(dsm + Ly.ringe);
   int32_t* plist = reinterpret_cast<int32_t*>(dsm + Ly.plist);   // prep: live-ish entries
   // control words: [0] chunks, [1] dropped entries, [2] prep list count,
-  // [3] walk request, [13] stopped for the next round, [14] re-run the
-  // chunk, [15] walk handed back
+  // [3] walk request, [16] stopped for the next round, [17] re-run the
+  // chunk, [18] walk handed back (int32 words; bytes 16..63 hold the
+  // 8-byte values below)
   volatile int32_t* ctl = reinterpret_cast<volatile int32_t*>(dsm + Ly.ctl);
   volatile double* pub_thr = reinterpret_cast<volatile double*>(dsm + Ly.ctl + 16);
   volatile long long* walk_from = reinterpret_cast<volatile long long*>(dsm + Ly.ctl + 24);
@@ -1032,7 +1098,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   }
   if (st.done) return;  // finished in an earlier round
   if (tid == 0) {
-    ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[13] = 0; ctl[14] = 0; ctl[15] = 0;
+    ctl[1] = 0; ctl[2] = 0; ctl[3] = 0; ctl[16] = 0; ctl[17] = 0; ctl[18] = 0;
     *sskip = st.P - 1;
   }
   __syncthreads();
@@ -1103,47 +1169,73 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   // Walk items [from, to) in order with the live threshold.  hand_back: stop
   // at the first insertion that brings the threshold back to <= theta (the
   // lists cover the rest).  Afterwards *sskip = the last decided item.
-  // Scratch: rmask holds sub/32 flag words, rlst 1024 positions.
+  // Sub-ranges are flagged by all four warps against the threshold T at
+  // their start, with coalesced 16-byte reads of the tile-transposed fast
+  // rows (a warp tile = 128 chunks; lane l holds the consecutive logical
+  // chunks 4l..4l+3); warp 0 decides the flagged items in order.  An
+  // insertion lifting the threshold above T restarts flagging right after
+  // it, with a short sub-range that doubles while no restart happens.
+  // Scratch: rmask holds max_sub/32 flag words, rlst 1024 positions.
   auto walk = [&](int64_t from, int64_t to, bool hand_back, uint32_t* rmask, int32_t* rlst,
-                  int sub) {
-    const int kSub = sub;  // items per flagged sub-range
+                  int max_sub) {
+    using G = FGeo<FP>;
+    constexpr int IPC = G::IPC, TILE = G::TILE;
+    constexpr int LB = 4 * IPC;                   // flag bits per lane and tile
+    constexpr int LPW = LB >= 32 ? 1 : 32 / LB;   // lanes per flag word
+    const int sub_cap = max_sub - TILE;           // (the first tile may start before s0)
+    int sub = hand_back ? min(8192, sub_cap) : sub_cap;
     int64_t s0 = from;
     bool back = false;
     while (s0 < to && !back) {
-      const int64_t s1 = min(to, s0 + (int64_t)kSub);
-      const int nsub = (int)(s1 - s0);
+      const int64_t s1 = min(to, s0 + (int64_t)sub);
+      const int64_t base = s0 & ~(int64_t)(TILE - 1);
       if (tid == 0) *tsub = (p.debug & 16) ? kInf64 : L.thr64;  // debug: flag every item
       __syncthreads();
       const double T = *tsub;
-      constexpr int kPW = 16;
-      // kPW words per warp and pass: the row reads of a pass overlap
-      for (int b0 = warp * 32 * kPW; b0 < nsub; b0 += kRW * 32 * kPW) {
-        Row rows[kPW];
+      const int ntile = (int)((s1 - base + TILE - 1) / TILE);
+      for (int t = warp; t < ntile; t += kRW) {
+        const int64_t tb = base + (int64_t)t * TILE;
+        const uint4* cp = reinterpret_cast<const uint4*>(p.codes_fast) + tb / IPC + lane;
+        uint4 x[4];
 #pragma unroll
-        for (int u = 0; u < kPW; ++u) {
-          const int x = b0 + u * 32 + lane;
-          if (x < nsub) rows[u] = load_fast_row(p.codes_fast, FP, s0 + x);
-        }
+        for (int v = 0; v < 4; ++v) x[v] = __ldg(cp + v * 32);
+        unsigned long long bits = 0;
+        const int64_t i0 = tb + (int64_t)lane * LB;  // this lane's first item
 #pragma unroll
-        for (int u = 0; u < kPW; ++u) {
-          const int x = b0 + u * 32 + lane;
-          bool under = false;
-          if (x < nsub) {
-            double f = 0.0;  // float64 fast score in the reference's order
+        for (int v = 0; v < 4; ++v) {
 #pragma unroll
-            for (int s2 = 0; s2 < FP; ++s2)
-              if (s2 < F) f = __dadd_rn(f, lutf[s2 * m + (int)rows[u].byte(s2)]);
-            under = !(f >= T);  // (T = inf: every item, NaN scores included)
+          for (int j = 0; j < IPC; ++j) {
+            const int64_t i = i0 + v * IPC + j;
+            double f;
+            if constexpr (FP <= 8) {
+              f = tuple_f64<FP>(chunk_tuple<FP>(x[v], j), lutf, m, F);
+            } else {
+              const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+              f = 0.0;  // float64 fast score in the reference's order
+#pragma unroll
+              for (int s2 = 0; s2 < FP; ++s2)
+                if (s2 < F) f = __dadd_rn(f, lutf[s2 * m + ((wd[s2 >> 2] >> (8 * (s2 & 3))) & 0xffu)]);
+            }
+            // (T = inf flags every item, NaN scores included)
+            if (i >= s0 && i < s1 && !(f >= T)) bits |= 1ull << (v * IPC + j);
           }
-          const uint32_t bw = __ballot_sync(kFull, under);
-          if (lane == 0 && b0 + u * 32 < nsub) rmask[(b0 >> 5) + u] = bw;
+        }
+        const int w0 = (int)((tb - base) >> 5);  // first flag word of the tile
+        if constexpr (LB >= 32) {
+#pragma unroll
+          for (int h = 0; h < LB / 32; ++h) rmask[w0 + lane * (LB / 32) + h] = (uint32_t)(bits >> (32 * h));
+        } else {
+          uint32_t wv = (uint32_t)bits << ((lane % LPW) * LB);
+#pragma unroll
+          for (int o = 1; o < LPW; o <<= 1) wv |= __shfl_xor_sync(kFull, wv, o);
+          if (lane % LPW == 0) rmask[w0 + lane / LPW] = wv;
         }
       }
       __syncthreads();
       if (warp == 0) {
         int64_t next = s1;
         bool hb = false;
-        const int nwords = (nsub + 31) >> 5;
+        const int nwords = ntile * (TILE / 32);
         for (int w0 = 0; w0 < nwords; w0 += 32) {
           const uint32_t wv = w0 + lane < nwords ? rmask[w0 + lane] : 0u;
           const int cw = __popc(wv);
@@ -1157,11 +1249,11 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           int o = incl - cw;
           for (uint32_t bb = wv; bb; bb &= bb - 1) rlst[o++] = (w0 + lane) * 32 + __ffs(bb) - 1;
           __syncwarp();
-          const int b = decide_items([&](int x) { return s0 + rlst[x]; }, nl, T,
+          const int b = decide_items([&](int x) { return base + rlst[x]; }, nl, T,
                                      hand_back ? theta : -kInf64);
           __syncwarp();
           if (b >= 0) {  // an insertion moved the threshold out of (floor, T]
-            const int64_t y = s0 + rlst[b];
+            const int64_t y = base + rlst[b];
             hb = hand_back && L.thr64 <= theta;
             next = hb ? y : y + 1;  // rose above T: flag again from the next item
             break;
@@ -1169,24 +1261,27 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         }
         if (lane == 0) {
           *snext = (long long)next;
-          ctl[15] = hb ? 1 : 0;
+          ctl[18] = hb ? 1 : 0;
           *pub_thr = L.thr64;
         }
       }
       __syncthreads();
-      back = ctl[15] != 0;
+      back = ctl[18] != 0;
       const int64_t nx = (int64_t)*snext;
-      if (tid == 0) walked += (back ? nx + 1 : nx) - s0;
+      walked += (back ? nx + 1 : nx) - s0;  // (CTA-uniform)
+      // restarted after an insertion: short sub-ranges again; else grow
+      sub = nx < s1 ? min(2048, sub_cap) : min(2 * sub, sub_cap);
       s0 = back ? nx + 1 : nx;
-      // a long walk is handed to the next round: the filter lists the rest
-      // under the current live threshold on all SMs (one CTA walks ~1 item
-      // per clock; a filter pass streams the whole query in microseconds)
-      if (hand_back && !back && !p.last_round && s0 < to && s0 - from > p.walk_cap) {
-        if (tid == 0) ctl[13] = 1;
+      // long walks (in-order and overflowed-slice walks of this round
+      // together) hand the query to the next round: the filter lists the
+      // rest under the current live threshold on all SMs (one CTA walks ~1
+      // item per clock; a filter pass streams the whole query in microseconds)
+      if (!back && !p.last_round && s0 < to && walked > p.walk_cap) {
+        if (tid == 0) ctl[16] = 1;
         break;
       }
     }
-    if (tid == 0) *sskip = (long long)((back || ctl[13]) ? s0 - 1 : max(to - 1, (int64_t)*sskip));
+    if (tid == 0) *sskip = (long long)((back || ctl[16]) ? s0 - 1 : max(to - 1, (int64_t)*sskip));
     __syncthreads();
   };
 
@@ -1199,7 +1294,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
     const int NS = p.NR * kFW;  // slices of this query, in database order
     const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
     const int ptid = tid - 32;  // preparing thread index (warps 1..3)
-    for (int g0 = 0; g0 < NS && *sskip < n - 1 && !ctl[13]; g0 += kSG) {
+    for (int g0 = 0; g0 < NS && *sskip < n - 1 && !ctl[16]; g0 += kSG) {
       const int ng = min(kSG, NS - g0);
       {  // group meta (counts + page ids) -> shared memory
         const int pieces = ng * kSliceInts / 4;
@@ -1338,7 +1433,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       __syncthreads();
       for (int ch = 0; ch < nc;) {
         const long long tw0 = clock64();
-        const bool rerun = ctl[14] != 0;  // (CTA-uniform: set before the last barrier)
+        const bool rerun = ctl[17] != 0;  // (CTA-uniform: set before the last barrier)
         const bool rescan = chunk[3 * ch + 2] >= 0;
         if (warp > 0) {
           if (!rerun) {
@@ -1387,7 +1482,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             // words, 64k-item sub-ranges) and exact-score slot are free)
             walk(lo, hi_, false, reinterpret_cast<uint32_t*>(ring + (ch % kRSlots) * kCH),
                  reinterpret_cast<int32_t*>(ring_e + (ch % kRSlots) * kCH), kCH * 16 * 8);
-            if (warp == 0 && lane == 0 && L.thr64 > theta && hi_ < n) {
+            if (warp == 0 && lane == 0 && L.thr64 > theta && hi_ < n && !ctl[16]) {
               *walk_from = hi_;  // the lists stop covering the items after the slice
               ctl[3] = 1;
             }
@@ -1405,23 +1500,23 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           // the iterations ch+1 / ch+2); 4 KiB each -> 32k-item sub-ranges
           walk(from, n, true, reinterpret_cast<uint32_t*>(ring_e + ((ch + 2) % kRSlots) * kCH),
                reinterpret_cast<int32_t*>(ring_e + ((ch + 3) % kRSlots) * kCH), kCH * 8 * 8);
-          if (tid == 0) ctl[14] = 1;  // decide the rest of chunk ch (ids after the walk)
+          if (tid == 0) ctl[17] = 1;  // decide the rest of chunk ch (ids after the walk)
           __syncthreads();
         } else {
-          if (tid == 0) ctl[14] = 0;
+          if (tid == 0) ctl[17] = 0;
           __syncthreads();
           ++ch;
         }
-        if (*sskip >= n - 1 || ctl[13]) break;  // (CTA-uniform) walked to the end / stopped
+        if (*sskip >= n - 1 || ctl[16]) break;  // (CTA-uniform) walked to the end / stopped
       }
       if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
-      if (tid == 0) ctl[14] = 0;
+      if (tid == 0) ctl[17] = 0;
       __syncthreads();
     }
     if (warp == 0) L.H.store(lane);
   }
   __syncthreads();
-  if (ctl[13]) {
+  if (ctl[16]) {
     // a walk ran past p.walk_cap: hand the query to the next round -- the
     // heap (sorted descending), the first undecided item and, as the new
     // list threshold, the live threshold itself (J = 0)

@@ -82,7 +82,9 @@ struct PipeParams {
   int32_t debug;              // experiments only (ICQ_DEBUG): bit 0 = no tuple-tie rejection,
                               // bit 1 = replay producers skip exact scores
   int32_t list_j;             // list threshold theta = A_J + sigma at the prologue end (A_J:
-                              // max fast score over the J+1 largest-exact heap entries)
+                              // max fast score over the J+1 largest-exact heap entries);
+                              // -1: the loosest J on a ladder with a list share <= 1/list_div
+  int32_t list_div;
   int32_t pro_live;           // prologue stop rule counts items under theta (1) or under M (0)
   int32_t sigma_f32;          // numpy promotion of a float32 sigma (see live_thr)
   int32_t rounds;             // filter/replay rounds (1..kMaxRounds)

@@ -83,8 +83,13 @@ CONFIGS = [
 #               theta = the live threshold at the prologue end; the replay
 #               decides the lists and walks the database in order whenever
 #               the live threshold rises above theta
-#   listj     - as filter, theta = A_5 + sigma (max fast over the 6 largest
-#               heap entries): longer lists, fewer walks
+#               (theta = A_J + sigma, A_J the max fast score over the J+1
+#               largest heap entries; J the loosest on a ladder whose share
+#               of the last prologue items is <= 1/128)
+#   listj     - as filter, J = 5 fixed
+#   listj0    - as filter, J = 0: theta = the live threshold (most walks)
+#   listdiv   - as filter, J chosen for a 1/4 share, 16-page pool: long
+#               lists that overflow their slices
 #   prolive   - as filter with a 16k-item cap, the prologue stop rule counts
 #               items under theta instead of the stale M
 #   overflow  - as filter, with a 2-page candidate pool: slices overflow and
@@ -104,6 +109,8 @@ MODES = {
     "default": {},
     "filter": dict(_F),
     "listj": dict(_F, ICQ_LIST_J="5"),
+    "listj0": dict(_F, ICQ_LIST_J="0"),
+    "listdiv": dict(_F, ICQ_LIST_DIV="4", ICQ_POOL_PAGES="16"),
     "prolive": {"ICQ_PRO_MAX": "16384", "ICQ_PRO_MIN": "0", "ICQ_PRO_LIVE": "1"},
     "overflow": dict(_F, ICQ_POOL_PAGES="2"),
     "subbatch": {"ICQ_PRO_MAX": "4096", "ICQ_PRO_MIN": "0", "ICQ_QBATCH": "4"},

@@ -91,6 +91,10 @@ def main():
     pct = lambda a: [float(np.percentile(a, p)) for p in (0, 50, 90, 99, 100)]
     print(json.dumps({nm: pct(v) for nm, v in S.items()} | {"refinements": pct(ref)}, indent=0))
     order = np.argsort(-S["replay_cycles"])
+    for qi in order[:12]:
+        print("heavy", int(qi), {nm: int(S[nm][qi]) for nm in STATS_NAMES}, "refined", int(ref[qi]))
+    if args.deep <= 0:
+        return
     pick = list(order[: args.deep]) + list(order[len(order) // 2: len(order) // 2 + 2])
     K = w.K
     fidx = torch.as_tensor(fast.astype(np.int64), device="cuda")
