@@ -34,7 +34,9 @@ typedef enum {
   ICQ_ERR_VALIDATION = 1,   /* -> icq.data.ValidationError (data.py:32) */
   ICQ_ERR_UNSUPPORTED = 2,  /* shape outside this build (m > 256, K > 16, k too large) */
   ICQ_ERR_CUDA = 3,         /* CUDA runtime / launch failure */
-  ICQ_ERR_NOMEM = 4         /* device allocation failed / workspace too small */
+  ICQ_ERR_NOMEM = 4,        /* device allocation failed / workspace too small */
+  ICQ_ERR_FORMAT = 5,       /* -> icq.data.FormatError (data.py:36): malformed ICQI file */
+  ICQ_ERR_VERSION = 6       /* -> icq.data.UnsupportedVersionError (data.py:40) */
 } icq_status;
 
 typedef struct icq_index_s* icq_index_t;
@@ -79,6 +81,49 @@ icq_status icq_index_create_device(const float* books_dev, int32_t K, int32_t m,
                                    void* stream, icq_index_t* out);
 
 icq_status icq_index_destroy(icq_index_t h);
+
+/* Copy rows [row0, row0 + rows) of the index's codes back to the host as
+ * uint8 (rows, K) row-major (the reference's CodeMatrix values). */
+icq_status icq_index_read_codes(icq_index_t h, int64_t row0, int64_t rows, uint8_t* codes_host);
+
+/* ---------------------------------------------------------------------------
+ * load_index (data.py:348-394) straight into device memory.
+ * icq_index_file_info_read parses and validates the header only (magic,
+ * version, Config, n, d).  icq_index_load validates the whole file with the
+ * reference's conditions (bad magic / truncation / inconsistent lengths /
+ * trailing bytes / invalid Config or SearchIndex fields -> ICQ_ERR_FORMAT,
+ * version != 1 -> ICQ_ERR_VERSION), then streams the (n, K) uint32 code
+ * block through pinned host buffers into the device repack (the block is
+ * never materialised whole).  Optional host outputs: books [K*m*d], xi [d],
+ * lambdas [d]; info gets the Config fields, the float32 margin and the fast
+ * set (flatnonzero of the file's fast mask).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t K, m, d, n;               /* Config.K, Config.m; u32 n, d */
+  double gamma1, gamma2, pi1, pi2, alpha2, sigma_scale;
+  int64_t epochs, batch_size;
+  double learning_rate;
+  uint64_t seed;
+  float sigma;                      /* the stored float32 margin (data.py:322) */
+  int32_t F;
+  uint32_t fast[64];
+  int64_t file_bytes;
+} icq_index_file_info;
+
+icq_status icq_index_file_info_read(const char* path, icq_index_file_info* info);
+icq_status icq_index_load(const char* path, float* books_host, uint8_t* xi_host,
+                          float* lambdas_host, icq_index_file_info* info, void* stream,
+                          icq_index_t* out);
+
+/* ---------------------------------------------------------------------------
+ * search_bruteforce (search.py:168-178): exact float64 squared Euclidean scan
+ * over raw float32 vectors, top-k by (score, id) -- bitwise the reference's
+ * scores (numpy pairwise order).  x_dev: float32 [n*d] row-major; q_dev:
+ * float64 [Q*d]; ids_dev int64 [Q*k]; scores_dev float64 [Q*k].  k <= 1024.
+ * ------------------------------------------------------------------------- */
+icq_status icq_bruteforce(const float* x_dev, int64_t n, int32_t d, const double* q_dev,
+                          int32_t Q, int32_t k, int64_t* ids_dev, double* scores_dev,
+                          void* stream);
 
 /* Shape and device footprint of an index. */
 icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int32_t* d,

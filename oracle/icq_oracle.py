@@ -277,3 +277,17 @@ def two_step_loop(books, codes, fast, sigma, q, k: int) -> OracleResult:
         ops=ops,
         survivors=np.asarray(survivors, dtype=np.int64),
     )
+
+
+def bruteforce(x, q, k: int) -> OracleResult:
+    """search_bruteforce, search.py:168-178: float64 direct difference over raw
+    vectors (numpy pairwise order along d), lexsort by (score, id)."""
+    x = np.asarray(x)
+    n, d = x.shape
+    check_k(k, n)
+    q = check_query(q, d)
+    diff = x.astype(np.float64) - q[None, :]
+    scores = (diff * diff).sum(axis=1)
+    order = np.lexsort((np.arange(n), scores))[:k]
+    ops = OracleOps(exact_adds=(d - 1) * n, evaluations=n, refinements=n)
+    return OracleResult(ids=order.astype(np.int64), scores=scores[order], ops=ops)

@@ -12,10 +12,22 @@ from .data import (
     CodeMatrix,
     Config,
     DeviceError,
+    EmbeddedDataset,
+    FormatError,
     SearchIndex,
     UnsupportedError,
+    UnsupportedVersionError,
     ValidationError,
 )
+from .evaluate import (
+    EvalReport,
+    average_precision,
+    code_length_bits,
+    effective_code_length,
+    recall_at,
+    run_benchmark,
+)
+from .io import DeviceSearchIndex, load_dataset, load_index, save_dataset, save_index
 from .search import (
     BatchResult,
     DeviceIndex,
@@ -25,6 +37,9 @@ from .search import (
     device_index,
     exact_score,
     fast_score,
+    DeviceDataset,
+    search_bruteforce,
+    search_bruteforce_batch,
     search_exact,
     search_exact_batch,
     search_two_step,
@@ -33,6 +48,23 @@ from .search import (
 
 __all__ = [
     "BatchResult",
+    "DeviceDataset",
+    "DeviceSearchIndex",
+    "EmbeddedDataset",
+    "EvalReport",
+    "FormatError",
+    "UnsupportedVersionError",
+    "average_precision",
+    "code_length_bits",
+    "effective_code_length",
+    "load_dataset",
+    "load_index",
+    "recall_at",
+    "run_benchmark",
+    "save_dataset",
+    "save_index",
+    "search_bruteforce",
+    "search_bruteforce_batch",
     "CodebookSet",
     "CodeMatrix",
     "Config",

@@ -19,6 +19,19 @@ ICQ_ERR_VALIDATION = 1
 ICQ_ERR_UNSUPPORTED = 2
 ICQ_ERR_CUDA = 3
 ICQ_ERR_NOMEM = 4
+ICQ_ERR_FORMAT = 5
+ICQ_ERR_VERSION = 6
+
+class IndexFileInfo(C.Structure):
+    """icq_index_file_info (include/icq_b200.h)."""
+
+    _fields_ = [("K", C.c_int64), ("m", C.c_int64), ("d", C.c_int64), ("n", C.c_int64),
+                ("gamma1", C.c_double), ("gamma2", C.c_double), ("pi1", C.c_double),
+                ("pi2", C.c_double), ("alpha2", C.c_double), ("sigma_scale", C.c_double),
+                ("epochs", C.c_int64), ("batch_size", C.c_int64),
+                ("learning_rate", C.c_double), ("seed", C.c_uint64), ("sigma", C.c_float),
+                ("F", C.c_int32), ("fast", C.c_uint32 * 64), ("file_bytes", C.c_int64)]
+
 
 # exported symbols and their C signatures (kept in sync with include/icq_b200.h)
 _vp = C.c_void_p
@@ -43,6 +56,11 @@ SIGNATURES = {
                                    _vp, C.POINTER(_i32), _vp]),
     "icq_search_host": (_i32, [_vp, _vp, _i32, _i32, C.c_double, _i32, _vp, _vp, _vp,
                                C.POINTER(_i32)]),
+    "icq_index_read_codes": (_i32, [_vp, _i64, _i64, _vp]),
+    "icq_index_file_info_read": (_i32, [C.c_char_p, C.POINTER(IndexFileInfo)]),
+    "icq_index_load": (_i32, [C.c_char_p, _vp, _vp, _vp, C.POINTER(IndexFileInfo), _vp,
+                              C.POINTER(_vp)]),
+    "icq_bruteforce": (_i32, [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp]),
     "icq_profile_enable": (_i32, [_i32]),
     "icq_profile_read": (_i32, [C.POINTER(C.c_double), C.POINTER(_i32)]),
 }

@@ -13,8 +13,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/icq_b200.h"
-#include "icq_common.cuh"
+#include "icq_index.cuh"
 
 
 using namespace icq;
@@ -27,40 +26,22 @@ static std::mutex g_prof_mu;
 static bool g_prof_on = false;
 static std::vector<cudaEvent_t> g_prof_events;  // groups of kProfEvents per batch
 
-static icq_status fail(icq_status code, const char* fmt, ...) {
+static inline icq_status fail_v(icq_status code, const char* fmt, va_list ap) {
   char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
   vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
   g_err = buf;
   return code;
 }
+#define fail icq_fail
 
-#define CUDA_TRY(expr)                                                                   \
-  do {                                                                                   \
-    cudaError_t _e = (expr);                                                             \
-    if (_e != cudaSuccess)                                                               \
-      return fail(ICQ_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
-                  __LINE__);                                                             \
-  } while (0)
+icq_status icq_fail(icq_status code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  const icq_status r = fail_v(code, fmt, ap);
+  va_end(ap);
+  return r;
+}
 
-struct icq_index_s {
-  int32_t K, m, d, F, KP, FP;
-  int64_t n, n_pad;
-  float* books;
-  uint8_t* codes_full;
-  uint8_t* codes_fast;   // fast books, tile-transposed (streamed by the filter)
-  uint8_t* codes_xfull;  // all books, tile-transposed (the exact engine's stream)
-  uint8_t fast_books[kMaxK];
-  LutProg* prog_dev;
-  int32_t* err_dev;
-  int64_t bytes;
-  // device scratch of the synchronous host-buffer path, reused across calls
-  std::mutex host_mu;
-  char* host_buf = nullptr;
-  size_t host_buf_bytes = 0;
-};
 
 static int pow2_ceil(int x) {
   int p = 1;
@@ -72,16 +53,17 @@ static int pow2_ceil(int x) {
 // repack: (n, K) codes -> uint8 full rows (stride KP) + fast rows (stride FP)
 // --------------------------------------------------------------------------
 template <typename CodeT>
-__global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t n, int K, int m, int KP,
-                              uint8_t* __restrict__ full, int FP, int F, const FastBooks fb,
-                              uint8_t* __restrict__ fastp, uint8_t* __restrict__ xfull,
-                              int32_t* err) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+__global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t row0, int64_t rows, int K,
+                              int m, int KP, uint8_t* __restrict__ full, int FP, int F,
+                              const FastBooks fb, uint8_t* __restrict__ fastp,
+                              uint8_t* __restrict__ xfull, int32_t* err) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t i = row0 + r;
   uint8_t row[kMaxK];
   bool bad = false;
   for (int b = 0; b < K; ++b) {
-    const uint64_t c = (uint64_t)codes[i * K + b];
+    const uint64_t c = (uint64_t)codes[r * K + b];
     bad |= c >= (uint64_t)m;
     row[b] = (uint8_t)c;
   }
@@ -97,10 +79,21 @@ __global__ void repack_kernel(const CodeT* __restrict__ codes, int64_t n, int K,
   for (int b = 0; b < KP; ++b) xd[b] = b < K ? row[b] : 0;
 }
 
-template <typename CodeT>
-static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t d,
-                              const CodeT* codes, int64_t n, const uint32_t* fast, int32_t F,
-                              bool on_device, cudaStream_t stream, icq_index_t* out) {
+void icq_index_free(icq_index_t h) {
+  if (!h) return;
+  cudaFree(h->books);
+  cudaFree(h->codes_full);
+  cudaFree(h->codes_fast);
+  cudaFree(h->codes_xfull);
+  cudaFree(h->prog_dev);
+  cudaFree(h->err_dev);
+  cudaFree(h->host_buf);
+  delete h;
+}
+
+icq_status icq_index_alloc(const float* books, bool books_on_device, int32_t K, int32_t m,
+                           int32_t d, int64_t n, const uint32_t* fast, int32_t F,
+                           cudaStream_t stream, icq_index_t* out) {
   if (!out) return fail(ICQ_ERR_VALIDATION, "out handle pointer is NULL");
   *out = nullptr;
   if (K < 1) return fail(ICQ_ERR_VALIDATION, "K must be >= 1, got %d", K);
@@ -126,20 +119,11 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
   h->FP = F ? pow2_ceil(F) : 0;
   h->n_pad = (n + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
   memset(h->fast_books, 0, sizeof(h->fast_books));
-  bool prefix = true;
+  memset(&h->fb, 0, sizeof(h->fb));
   for (int s = 0; s < F; ++s) {
     h->fast_books[s] = (uint8_t)fast[s];
-    prefix &= fast[s] == (uint32_t)s;
+    h->fb.b[s] = (uint8_t)fast[s];
   }
-  (void)prefix;
-
-  auto cleanup = [&](icq_status st) {
-    cudaFree(h->books); cudaFree(h->codes_full);
-    cudaFree(h->codes_fast); cudaFree(h->codes_xfull);
-    cudaFree(h->prog_dev); cudaFree(h->err_dev);
-    delete h;
-    return st;
-  };
   const size_t bbytes = (size_t)K * m * d * sizeof(float);
   const size_t fullb = (size_t)h->n_pad * h->KP;
   const size_t fastb = F ? (size_t)h->n_pad * h->FP : 0;
@@ -150,52 +134,74 @@ static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t 
       (e = cudaMalloc(&h->codes_xfull, fullb)) != cudaSuccess ||
       (e = cudaMalloc(&h->prog_dev, sizeof(LutProg))) != cudaSuccess ||
       (e = cudaMalloc(&h->err_dev, sizeof(int32_t))) != cudaSuccess) {
-    fail(ICQ_ERR_NOMEM, "device allocation failed: %s", cudaGetErrorString(e));
-    return cleanup(ICQ_ERR_NOMEM);
+    icq_index_free(h);
+    return fail(ICQ_ERR_NOMEM, "device allocation failed: %s", cudaGetErrorString(e));
   }
   h->bytes = (int64_t)(bbytes + 2 * fullb + fastb);
+  const cudaMemcpyKind kind = books_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if ((e = cudaMemcpyAsync(h->books, books, bbytes, kind, stream)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(h->prog_dev, &prog, sizeof(LutProg), cudaMemcpyHostToDevice, stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(h->err_dev, 0, sizeof(int32_t), stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(h->codes_full, 0, fullb, stream)) != cudaSuccess ||
+      (fastb && (e = cudaMemsetAsync(h->codes_fast, 0, fastb, stream)) != cudaSuccess) ||
+      (e = cudaMemsetAsync(h->codes_xfull, 0, fullb, stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(stream)) != cudaSuccess) {  // (books may be a transient host buffer)
+    icq_index_free(h);
+    return fail(ICQ_ERR_CUDA, "index upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return ICQ_OK;
+}
 
+cudaError_t icq_index_repack_rows(icq_index_t h, const void* codes_dev, int code_bytes,
+                                  int64_t row0, int64_t rows, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((rows + threads - 1) / threads);
+  if (code_bytes == 4)
+    repack_kernel<uint32_t><<<blocks, threads, 0, s>>>(
+        static_cast<const uint32_t*>(codes_dev), row0, rows, h->K, h->m, h->KP, h->codes_full,
+        h->FP, h->F, h->fb, h->F ? h->codes_fast : nullptr, h->codes_xfull, h->err_dev);
+  else
+    repack_kernel<uint8_t><<<blocks, threads, 0, s>>>(
+        static_cast<const uint8_t*>(codes_dev), row0, rows, h->K, h->m, h->KP, h->codes_full,
+        h->FP, h->F, h->fb, h->F ? h->codes_fast : nullptr, h->codes_xfull, h->err_dev);
+  return cudaGetLastError();
+}
+
+// 0 = ok, else the error word (bit 1: a code >= m)
+int32_t icq_index_repack_errors(icq_index_t h) {
+  int32_t err = 0;
+  if (cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return err;
+}
+
+template <typename CodeT>
+static icq_status create_impl(const float* books, int32_t K, int32_t m, int32_t d,
+                              const CodeT* codes, int64_t n, const uint32_t* fast, int32_t F,
+                              bool on_device, cudaStream_t stream, icq_index_t* out) {
+  icq_index_t h = nullptr;
+  icq_status st = icq_index_alloc(books, on_device, K, m, d, n, fast, F, stream, &h);
+  if (st != ICQ_OK) return st;
   const CodeT* codes_dev = codes;
   CodeT* staged = nullptr;
-  auto run = [&]() -> cudaError_t {
-    cudaError_t e2;
-    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    if ((e2 = cudaMemcpyAsync(h->books, books, bbytes, kind, stream)) != cudaSuccess) return e2;
-    if ((e2 = cudaMemcpyAsync(h->prog_dev, &prog, sizeof(LutProg), cudaMemcpyHostToDevice,
-                              stream)) != cudaSuccess) return e2;
-    if ((e2 = cudaMemsetAsync(h->err_dev, 0, sizeof(int32_t), stream)) != cudaSuccess) return e2;
-    if ((e2 = cudaMemsetAsync(h->codes_full, 0, fullb, stream)) != cudaSuccess) return e2;
-    if (fastb && (e2 = cudaMemsetAsync(h->codes_fast, 0, fastb, stream)) != cudaSuccess) return e2;
-    if ((e2 = cudaMemsetAsync(h->codes_xfull, 0, fullb, stream)) != cudaSuccess) return e2;
-    if (!on_device) {
-      const size_t cb = (size_t)n * K * sizeof(CodeT);
-      if ((e2 = cudaMalloc(&staged, cb)) != cudaSuccess) return e2;
-      if ((e2 = cudaMemcpyAsync(staged, codes, cb, cudaMemcpyHostToDevice, stream)) != cudaSuccess)
-        return e2;
-      codes_dev = staged;
-    }
-    FastBooks fb;
-    memset(&fb, 0, sizeof(fb));
-    for (int s = 0; s < F; ++s) fb.b[s] = (uint8_t)fast[s];
-    const int threads = 256;
-    const unsigned blocks = (unsigned)((n + threads - 1) / threads);
-    repack_kernel<CodeT><<<blocks, threads, 0, stream>>>(
-        codes_dev, n, K, m, h->KP, h->codes_full, h->FP, F, fb,
-        F ? h->codes_fast : nullptr, h->codes_xfull, h->err_dev);
-    if ((e2 = cudaGetLastError()) != cudaSuccess) return e2;
-    return cudaStreamSynchronize(stream);
-  };
-  e = run();
+  cudaError_t e = cudaSuccess;
+  if (!on_device) {
+    const size_t cb = (size_t)n * K * sizeof(CodeT);
+    if ((e = cudaMalloc(&staged, cb)) == cudaSuccess)
+      e = cudaMemcpyAsync(staged, codes, cb, cudaMemcpyHostToDevice, stream);
+    codes_dev = staged;
+  }
+  if (e == cudaSuccess) e = icq_index_repack_rows(h, codes_dev, (int)sizeof(CodeT), 0, n, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
   if (staged) cudaFree(staged);
   if (e != cudaSuccess) {
-    fail(ICQ_ERR_CUDA, "index upload/repack failed: %s", cudaGetErrorString(e));
-    return cleanup(ICQ_ERR_CUDA);
+    icq_index_free(h);
+    return fail(ICQ_ERR_CUDA, "index upload/repack failed: %s", cudaGetErrorString(e));
   }
-  int32_t err = 0;
-  cudaMemcpy(&err, h->err_dev, sizeof(err), cudaMemcpyDeviceToHost);
-  if (err & 2) {
-    fail(ICQ_ERR_VALIDATION, "codes reference codewords beyond m");
-    return cleanup(ICQ_ERR_VALIDATION);
+  if (icq_index_repack_errors(h) & 2) {
+    icq_index_free(h);
+    return fail(ICQ_ERR_VALIDATION, "codes reference codewords beyond m");
   }
   *out = h;
   g_err.clear();
@@ -254,15 +260,19 @@ icq_status icq_index_create_device(const float* books, int32_t K, int32_t m, int
 }
 
 icq_status icq_index_destroy(icq_index_t h) {
-  if (!h) return ICQ_OK;
-  cudaFree(h->books);
-  cudaFree(h->codes_full);
-  cudaFree(h->codes_fast);
-  cudaFree(h->codes_xfull);
-  cudaFree(h->prog_dev);
-  cudaFree(h->err_dev);
-  cudaFree(h->host_buf);
-  delete h;
+  icq_index_free(h);
+  return ICQ_OK;
+}
+
+icq_status icq_index_read_codes(icq_index_t h, int64_t row0, int64_t rows, uint8_t* codes_host) {
+  if (!h) return fail(ICQ_ERR_VALIDATION, "null index handle");
+  if (row0 < 0 || rows < 0 || row0 + rows > h->n)
+    return fail(ICQ_ERR_VALIDATION, "rows [%lld, %lld) outside [0, %lld)", (long long)row0,
+                (long long)(row0 + rows), (long long)h->n);
+  if (rows == 0) return ICQ_OK;
+  // codes_full rows are KP wide: copy the K leading bytes of each row
+  CUDA_TRY(cudaMemcpy2D(codes_host, (size_t)h->K, h->codes_full + row0 * h->KP, (size_t)h->KP,
+                        (size_t)h->K, (size_t)rows, cudaMemcpyDeviceToHost));
   return ICQ_OK;
 }
 

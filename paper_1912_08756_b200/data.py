@@ -79,11 +79,58 @@ class Config:
     learning_rate: float = 1e-2
     seed: int = 0
 
-    def __post_init__(self):
+    def __post_init__(self):  # data.py:102-122
         if self.K < 1:
             raise ValidationError(f"K must be >= 1, got {self.K}")
         if self.m < 2:
             raise ValidationError(f"m must be >= 2, got {self.m}")
+        if self.gamma1 < 0 or self.gamma2 < 0:
+            raise ValidationError("gamma1 and gamma2 must be non-negative")
+        if not (self.pi1 > self.pi2 > 0):
+            raise ValidationError(f"need pi1 > pi2 > 0, got {self.pi1}, {self.pi2}")
+        if abs(self.pi1 + self.pi2 - 1.0) > 1e-12:
+            raise ValidationError(f"pi1 + pi2 must equal 1, got {self.pi1 + self.pi2}")
+        if self.alpha2 >= 0:
+            raise ValidationError(f"alpha2 must be negative, got {self.alpha2}")
+        if self.sigma_scale < 0:
+            raise ValidationError(f"sigma_scale must be >= 0, got {self.sigma_scale}")
+        if self.epochs < 1 or self.batch_size < 1:
+            raise ValidationError("epochs and batch_size must be >= 1")
+        if self.learning_rate <= 0:
+            raise ValidationError(f"learning_rate must be > 0, got {self.learning_rate}")
+        if self.seed < 0:
+            raise ValidationError(f"seed must be >= 0, got {self.seed}")
+
+
+@dataclass
+class EmbeddedDataset:
+    """Vectors plus optional labels (data.py:44-77): (n, d) float32, (n,) uint32."""
+
+    vectors: np.ndarray
+    labels: np.ndarray | None = None
+
+    def __post_init__(self):
+        vectors = np.ascontiguousarray(self.vectors, dtype=np.float32)
+        if vectors.ndim != 2:
+            raise ValidationError(f"vectors must be 2-d, got shape {vectors.shape}")
+        self.vectors = vectors
+        if self.labels is not None:
+            labels = np.asarray(self.labels)
+            if labels.shape != (vectors.shape[0],):
+                raise ValidationError(
+                    f"labels shape {labels.shape} does not match n={vectors.shape[0]}")
+            if labels.size and (np.any(labels < 0)
+                                or not np.issubdtype(labels.dtype, np.integer)):
+                raise ValidationError("labels must be non-negative integers")
+            self.labels = np.ascontiguousarray(labels, dtype=np.uint32)
+
+    @property
+    def n(self) -> int:
+        return self.vectors.shape[0]
+
+    @property
+    def d(self) -> int:
+        return self.vectors.shape[1]
 
 
 @dataclass

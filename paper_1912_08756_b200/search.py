@@ -196,9 +196,27 @@ class DeviceIndex:
         self._fin = weakref.finalize(self, L.icq_index_destroy, h)
         return self
 
+    @classmethod
+    def _adopt(cls, h, K: int, m: int, d: int, n: int, F: int):
+        """Own an icq_index_t created elsewhere (icq_index_load)."""
+        self = cls.__new__(cls)
+        self._h = h
+        self.K, self.m, self.d, self.n, self.F = K, m, d, n, F
+        self._fin = weakref.finalize(self, _native.lib().icq_index_destroy, h)
+        return self
+
     @property
     def handle(self):
         return self._h
+
+    def read_codes(self, row0: int = 0, rows: int | None = None) -> np.ndarray:
+        """(rows, K) uint8 codes back from the device."""
+        rows = self.n - row0 if rows is None else rows
+        out = np.empty((rows, self.K), dtype=np.uint8)
+        st = _native.lib().icq_index_read_codes(self._h, row0, rows, out.ctypes.data)
+        if st != _native.ICQ_OK:
+            _raise(st, "icq_index_read_codes")
+        return out
 
     def search_lut_device(self, lut, k: int, sigma: float = 0.0, exact: bool = False, out=None,
                           stats=False, stream=None, survivors=False):
@@ -331,6 +349,9 @@ _cache_lock = threading.Lock()
 
 def device_index(index) -> DeviceIndex:
     """The DeviceIndex for a (reference or local) SearchIndex, uploaded once."""
+    dev = getattr(index, "_device", None)  # io.load_index: already on the device
+    if isinstance(dev, DeviceIndex):
+        return dev
     books = index.books.codewords
     codes = index.codes.codes
     fast = np.asarray(index.fast)
@@ -449,3 +470,86 @@ def search_exact_batch(index, queries, k: int) -> BatchResult:
     n = index.n
     return BatchResult(ids=ids, scores=scores, refinements=np.full(Q.shape[0], n, dtype=np.int64),
                        ops=[_ops_exact(index) for _ in range(Q.shape[0])])
+
+
+# ---------------------------------------------------------------------------
+# brute-force ground truth (search.py:168-178)
+# ---------------------------------------------------------------------------
+class DeviceDataset:
+    """Raw float32 vectors resident on the device (the brute-force scan's input)."""
+
+    def __init__(self, vectors):
+        import torch
+
+        if isinstance(vectors, torch.Tensor):
+            x = vectors
+            if x.dtype != torch.float32 or x.dim() != 2:
+                raise ValidationError("vectors must be a float32 (n, d) tensor")
+            self.x = x.contiguous() if x.is_cuda else x.contiguous().cuda()
+        else:
+            x = np.ascontiguousarray(np.asarray(vectors), dtype=np.float32)
+            if x.ndim != 2:
+                raise ValidationError(f"vectors must be 2-d, got shape {x.shape}")
+            self.x = torch.from_numpy(x).cuda()
+        self.n, self.d = int(self.x.shape[0]), int(self.x.shape[1])
+
+    def search_device(self, q, k: int, stream=None):
+        """Batched scan: q torch float64 (nq, d) on cuda -> ids (nq, k), scores (nq, k)."""
+        import torch
+
+        _check_k(k, self.n)
+        if q.dtype != torch.float64 or q.dim() != 2 or q.shape[1] != self.d or not q.is_cuda:
+            raise ValidationError("q must be a cuda float64 tensor of shape (nq, d)")
+        q = q.contiguous()
+        nq = q.shape[0]
+        ids = torch.empty((nq, k), dtype=torch.int64, device=q.device)
+        scores = torch.empty((nq, k), dtype=torch.float64, device=q.device)
+        s = stream if stream is not None else torch.cuda.current_stream(q.device).cuda_stream
+        st = _native.lib().icq_bruteforce(self.x.data_ptr(), self.n, self.d, q.data_ptr(), nq, k,
+                                          ids.data_ptr(), scores.data_ptr(), s)
+        if st != _native.ICQ_OK:
+            _raise(st, "icq_bruteforce")
+        return {"ids": ids, "scores": scores}
+
+
+_ds_cache: dict = {}
+
+
+def _device_dataset(ds) -> DeviceDataset:
+    if isinstance(ds, DeviceDataset):
+        return ds
+    x = ds.vectors if hasattr(ds, "vectors") else np.asarray(ds)
+    key = id(x)
+    hit = _ds_cache.get(key)
+    if hit is not None and hit[0] is x:
+        return hit[1]
+    dd = DeviceDataset(x)
+    _ds_cache.clear()  # one raw dataset at a time (they are large)
+    _ds_cache[key] = (x, dd)
+    return dd
+
+
+def search_bruteforce(ds, q, k: int) -> QueryResult:
+    """Exact squared Euclidean scan over raw vectors (search.py:168-178), on the GPU."""
+    import torch
+
+    dd = _device_dataset(ds)
+    _check_k(k, dd.n)
+    q = _check_query(q, dd.d)
+    out = dd.search_device(torch.from_numpy(q[None]).cuda(), k)
+    ops = OpCounter(exact_adds=(dd.d - 1) * dd.n, evaluations=dd.n, refinements=dd.n)
+    return QueryResult(ids=out["ids"][0].cpu().numpy(), scores=out["scores"][0].cpu().numpy(),
+                       ops=ops)
+
+
+def search_bruteforce_batch(ds, queries, k: int) -> BatchResult:
+    import torch
+
+    dd = _device_dataset(ds)
+    _check_k(k, dd.n)
+    Q = _check_queries(queries, dd.d)
+    out = dd.search_device(torch.from_numpy(Q).cuda(), k)
+    ops = [OpCounter(exact_adds=(dd.d - 1) * dd.n, evaluations=dd.n, refinements=dd.n)
+           for _ in range(Q.shape[0])]
+    return BatchResult(ids=out["ids"].cpu().numpy(), scores=out["scores"].cpu().numpy(),
+                       refinements=np.full(Q.shape[0], dd.n, dtype=np.int64), ops=ops)
