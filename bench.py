@@ -229,7 +229,8 @@ def main():
     fast, sigma, rule, sigma_rule = index_rule(w, meta, args.sigma)
 
     t0 = time.time()
-    codes = build_database(w, books, sweeps=args.sweeps)
+    enc_stats = {}
+    codes = build_database(w, books, sweeps=args.sweeps, stats=enc_stats)
     Qall = queries(w)
     torch.cuda.synchronize()
     prep_s = time.time() - t0
@@ -244,7 +245,9 @@ def main():
         "books": f"reference icq.train on {int(meta['train_rows'])} seeded rows, "
                  f"{int(meta['epochs'])} epoch(s), seed {int(meta['seed'])}",
         "seeds": {"train": SEED_TRAIN, "db": SEED_DB, "queries": SEED_QUERIES},
-        "encode": f"GPU ICM (greedy + <= {args.sweeps} sweeps, fp32)",
+        "encode": (f"GPU float64 ICM encoder (icq_encode: reference assign_codes, greedy + "
+                   f"<= {args.sweeps} sweeps; {enc_stats.get('sweeps_used')} used; "
+                   f"{enc_stats.get('encode_seconds', 0):.1f} s for {w.n} rows)"),
         "l2": "flushed (256 MiB write) before every timed step",
         "parallelism": f"replicas{world}" if world > 1 else "single",
     }
@@ -299,10 +302,10 @@ def main():
     L.icq_profile_enable(0)
     import ctypes as _C
 
-    kms = (_C.c_double * 3)()
+    kms = (_C.c_double * 4)()
     klaunch = _C.c_int32()
     L.icq_profile_read(kms, _C.byref(klaunch))
-    t_pro_k, t_filter_k, t_replay_k = (x / 1e3 for x in kms)
+    t_pro_k, t_filter_k, t_replay_k, t_count_k = (x / 1e3 for x in kms)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -445,7 +448,8 @@ def main():
         "kernels_ms_per_step": {"lut": t_lut / args.steps * 1e3,
                                 "prologue": t_pro_k / args.steps * 1e3,
                                 "filter": t_filter_k / args.steps * 1e3,
-                                "replay": t_replay_k / args.steps * 1e3},
+                                "replay": t_replay_k / args.steps * 1e3,
+                                "count": t_count_k / args.steps * 1e3},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": 4 * args.steps,

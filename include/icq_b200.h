@@ -125,6 +125,21 @@ icq_status icq_bruteforce(const float* x_dev, int64_t n, int32_t d, const double
                           int32_t Q, int32_t k, int64_t* ids_dev, double* scores_dev,
                           void* stream);
 
+/* ---------------------------------------------------------------------------
+ * assign_codes / encode_dataset (train.py:196-243, :256-274): ICM encoding in
+ * float64 on the device -- greedy build-up (codes_in_dev NULL) or sweeps
+ * from given codes, then up to max_sweeps strict-improvement sweeps, stopping
+ * after a sweep that changes nothing.  x_dev float32 [n*d]; books_dev
+ * float64 [K*m*d]; c_sq_dev float64 [K*m] (sum of squares over d in numpy's
+ * order); codes uint8 [n*K] (m <= 256).  sweeps_out: sweeps run (max over
+ * row chunks).  Codes equal the reference's except where two codewords tie
+ * to rounding (the reference's dgemm sums in a different order).
+ * ------------------------------------------------------------------------- */
+icq_status icq_encode(const float* x_dev, int64_t n, int32_t d, const double* books_dev,
+                      const double* c_sq_dev, int32_t K, int32_t m, const uint8_t* codes_in_dev,
+                      int32_t max_sweeps, uint8_t* codes_out_dev, int32_t* sweeps_out,
+                      void* stream);
+
 /* Shape and device footprint of an index. */
 icq_status icq_index_info(icq_index_t h, int64_t* n, int32_t* K, int32_t* m, int32_t* d,
                           int32_t* F, int64_t* device_bytes);
@@ -202,9 +217,10 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
 /* ---------------------------------------------------------------------------
  * Instrumentation (bench / profiling only; not part of the reference surface).
  * icq_profile_enable(1) makes every following search call record CUDA events
- * on its launch stream around the three kernels of each batch (prologue,
- * filter, replay).  icq_profile_read synchronizes those events and returns
- * the summed device milliseconds per kernel (ms_out[3]) and the number of
+ * on its launch stream around the kernels of each batch (prologue, filter
+ * and replay of every round, refinement count).  icq_profile_read
+ * synchronizes those events and returns the summed device milliseconds per
+ * kernel kind (ms_out[4]: prologue, filter, replay, count) and the number of
  * batches recorded, then clears the record.
  * ------------------------------------------------------------------------- */
 icq_status icq_profile_enable(int32_t on);

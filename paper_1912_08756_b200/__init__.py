@@ -27,6 +27,7 @@ from .evaluate import (
     recall_at,
     run_benchmark,
 )
+from .encode import assign_codes, encode_dataset, encode_device
 from .io import DeviceSearchIndex, load_dataset, load_index, save_dataset, save_index
 from .search import (
     BatchResult,
@@ -50,6 +51,9 @@ __all__ = [
     "BatchResult",
     "DeviceDataset",
     "DeviceSearchIndex",
+    "assign_codes",
+    "encode_dataset",
+    "encode_device",
     "EmbeddedDataset",
     "EvalReport",
     "FormatError",

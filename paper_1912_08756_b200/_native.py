@@ -61,6 +61,8 @@ SIGNATURES = {
     "icq_index_load": (_i32, [C.c_char_p, _vp, _vp, _vp, C.POINTER(IndexFileInfo), _vp,
                               C.POINTER(_vp)]),
     "icq_bruteforce": (_i32, [_vp, _i64, _i32, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "icq_encode": (_i32, [_vp, _i64, _i32, _vp, _vp, _i32, _i32, _vp, _i32, _vp,
+                          C.POINTER(_i32), _vp]),
     "icq_profile_enable": (_i32, [_i32]),
     "icq_profile_read": (_i32, [C.POINTER(C.c_double), C.POINTER(_i32)]),
 }

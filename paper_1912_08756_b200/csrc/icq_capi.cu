@@ -220,7 +220,7 @@ icq_status icq_profile_enable(int32_t on) {
 
 icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   std::lock_guard<std::mutex> g(g_prof_mu);
-  double acc[3] = {0, 0, 0};  // prologue, filter, replay
+  double acc[4] = {0, 0, 0, 0};  // prologue, filter, replay, count
   const int groups = (int)(g_prof_events.size() / kProfEvents);
   for (int i = 0; i < groups; ++i) {
     cudaEvent_t* e = &g_prof_events[kProfEvents * i];
@@ -229,12 +229,12 @@ icq_status icq_profile_read(double* ms_out, int32_t* launches) {
     for (int j = 0; j + 1 < kProfEvents; ++j) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e[j], e[j + 1]);
-      acc[j == 0 ? 0 : (j % 2 == 1 ? 1 : 2)] += ms;
+      acc[j == 0 ? 0 : (j == kProfEvents - 2 ? 3 : (j % 2 == 1 ? 1 : 2))] += ms;
     }
   }
   for (cudaEvent_t e : g_prof_events) cudaEventDestroy(e);
   g_prof_events.clear();
-  if (ms_out) for (int j = 0; j < 3; ++j) ms_out[j] = acc[j];
+  if (ms_out) for (int j = 0; j < 4; ++j) ms_out[j] = acc[j];
   if (launches) *launches = groups;
   return ICQ_OK;
 }
@@ -294,6 +294,7 @@ static icq_status check_call_errors(int32_t err) {
   if (err & 8) return fail(ICQ_ERR_VALIDATION, "query contains non-finite values");
   if (err & 1) return fail(ICQ_ERR_CUDA, "filter kernel shared-memory layout check failed");
   if (err & 4) return fail(ICQ_ERR_CUDA, "replay dropped candidate chunks");
+  if (err & 16) return fail(ICQ_ERR_CUDA, "count mode: more than %d insertions after the prologue", kMaxTraj);
   if (err) return fail(ICQ_ERR_CUDA, "device error word 0x%x", err);
   return ICQ_OK;
 }
@@ -422,6 +423,11 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   p.list_j = (int32_t)env_i("ICQ_LIST_J", -1);
   p.list_div = (int32_t)env_i("ICQ_LIST_DIV", 128);
   p.pro_live = (int32_t)env_i("ICQ_PRO_LIVE", 0);
+  // count mode (refinement-heavy queries: the live threshold passes > 1/count_div
+  // of the sampled items): lists of possible insertions + a parallel count
+  p.count_div = exact ? 0 : (int32_t)env_i("ICQ_COUNT_DIV", 128);
+  p.force_count = exact ? 0 : (int32_t)env_i("ICQ_COUNT_MODE", 0);
+  p.count_used = (FP <= 8 && (p.count_div > 0 || p.force_count)) ? 1 : 0;
   {
     const int64_t r = env_i("ICQ_ROUNDS", kMaxRounds);
     p.rounds = (int32_t)(r < 1 ? 1 : (r > kMaxRounds ? kMaxRounds : r));
@@ -468,7 +474,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   const size_t b_pool = al((size_t)p.pool_pages * kPG * sizeof(uint4));
   const size_t b_top = 256;  // pool_top, error word
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
-  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl;
+  const size_t b_tr = p.count_used ? al((size_t)Qb * kMaxTraj * sizeof(TrajEntry)) : 0;
+  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl + b_tr;
   char* sc = nullptr;
   CUDA_TRY(cudaMallocAsync((void**)&sc, scratch, s));
   {
@@ -481,7 +488,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.pool_top = reinterpret_cast<int32_t*>(o);
     p.error = p.pool_top + 1;
     o += b_top;
-    p.slices = reinterpret_cast<int32_t*>(o);
+    p.slices = reinterpret_cast<int32_t*>(o); o += b_sl;
+    p.traj = b_tr ? reinterpret_cast<TrajEntry*>(o) : nullptr;
   }
   (void)b_lut;
   icq_status st = ICQ_OK;

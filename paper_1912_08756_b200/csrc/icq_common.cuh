@@ -276,6 +276,7 @@ struct Live {
   double T64, bound64, thr64;
   float lo, hi;
   int64_t refinements, insertions, candidates, certified;
+  int32_t ntraj;  // count mode: trajectory entries recorded
   WarpHeap H;
 };
 

@@ -58,7 +58,10 @@ struct RCtx {
   double sigma;
   bool f32;  // numpy float32-sigma promotion (live_thr)
   bool pw, wide;
+  bool count_mode;  // decide insertions only; record the threshold trajectory
   uint32_t* surv;
+  TrajEntry* traj;
+  int32_t* error;
 };
 
 struct Decided {
@@ -499,7 +502,8 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   //     cost walks whenever the live threshold rises above theta (in order,
   //     one CTA).  ICQ_LIST_J >= 0 fixes J.
   int listJ = p.list_j;
-  if (listJ < 0) {
+  bool count_mode = FP <= 8 && p.force_count != 0 && !wide && pos < n;
+  if (listJ < 0 || p.count_div > 0) {
     constexpr int kLad = 9;
     const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30};
     float* lad_hi = reinterpret_cast<float*>(cf);        // (cf/ce are free now)
@@ -551,23 +555,41 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       if (lane == 0 && c2) atomicAdd(&lad_cnt[r], c2);
     }
     __syncthreads();
-    listJ = 0;
-    for (int r = 0; r < kLad; ++r)
-      if (S > 0 && (int64_t)lad_cnt[r] * p.list_div <= S) listJ = ladder[r];
+    if (p.list_j < 0) {
+      listJ = 0;
+      for (int r = 0; r < kLad; ++r)
+        if (S > 0 && (int64_t)lad_cnt[r] * p.list_div <= S) listJ = ladder[r];
+    }
     listJ = min(listJ, k - 1);
+    // refinement-heavy: even the live threshold passes > 1/count_div of the
+    // sample -> the lists would hold the refined items themselves
+    if (FP <= 8 && p.count_div > 0 && S > 0 && (int64_t)lad_cnt[0] * p.count_div > S)
+      count_mode = true;
     __syncthreads();
   }
   if (warp == 0) {
     int best = 0;
     const double A = heap_AJ(hf, k, listJ, lane, &best);
     double thr = wide ? kInf64 : thr_cover(A, p.sigma, f32s, false);
+    float hiT = kInf;
+    if (count_mode) {
+      // the lists keep every possible insertion, whatever sigma: an item
+      // inserted later has exact < T_P (T never increases), hence
+      // fast < T_P - Smin (its slow part is >= Smin); float64 slack for the
+      // different summation orders of fast and exact scores
+      const double sm = smin_rd(lut, K, m, p.fast_books, F, lane);
+      const double T = he[0];
+      thr = __dadd_ru(__dsub_ru(T, sm), fabs(T) * 1e-12);
+      float loT;
+      certified_bounds(T, K, loT, hiT);
+    }
     float flo = kInf, fhi = kInf;
     if (!wide) certified_bounds(thr, F, flo, fhi);
     // tie rejection costs the filter a tuple compare per candidate: enabled
     // only where the prologue saw near-ties in bulk (few-codeword books);
     // items with the threshold item's fast-code tuple tie at thr exactly
     const bool ties = (int64_t)(*band_total) * 2048 > pos && !(p.debug & 1);
-    const bool ok = ties && FP <= 8 && p.sigma == 0.0 && !f32s && !wide;
+    const bool ok = ties && FP <= 8 && p.sigma == 0.0 && !f32s && !wide && !count_mode;
     uint2 tup = make_uint2(0u, 0u);
     if (ok && lane == 0) {
       const Row r = load_fast_row(p.codes_fast, FP, hi[best]);
@@ -594,6 +616,11 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       st.done = 0;
       st.rounds = 0;
       st.walked = 0;
+      st.count_mode = count_mode ? 1 : 0;
+      st.hiT = hiT;
+      st.ntraj = 0;
+      st.thr0 = live_thr(hf[0], hi[0], p.sigma, k, f32s);
+      st.P0 = pos;
       st.ovf_pages = 0;
       st.ovf_pool = 0;
       st.skipped = 0;
@@ -659,6 +686,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
+  // count mode: float32 table of every book ([K][m], after lut64f, below the first page)
+  float* lut32k = reinterpret_cast<float*>(dsm + al16((uint32_t)(FP <= 8 ? FP : 8) * 256 * 8));
   const uint32_t two = 2u + (uint32_t)(p.n < 0);    // 2, opaque to the compiler (keeps IMADs)
   const uint32_t lt_mask = (1u << lane) - 1u;
   int cur_q = -1;
@@ -672,6 +701,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const uint2 mtup = make_uint2(p.qs[q].mtup[0], p.qs[q].mtup[1]);
     const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
+    const bool cmode = FP <= 8 && p.qs[q].count_mode != 0;
+    const float hiT = p.qs[q].hiT;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
     if (P >= r_hi || p.qs[q].done) {  // decided by the prologue / an earlier round
@@ -698,6 +729,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         const int s = i / m, j = i - s * m;
         lut64f[i] = glut[p.fast_books[s] * m + j];
       }
+      if (FP <= 8 && p.qs[q].count_mode)
+        for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
       __syncthreads();
       cur_q = q;
     }
@@ -841,6 +874,35 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
               b &= b - 1;
               const uint2 tj = chunk_tuple<FP>(x[v], j);
               if (tj.x == mtup.x && tj.y == mtup.y) cm &= ~((Mask)1 << (v * IPC + j));
+            }
+          }
+        }
+      }
+      if constexpr (FP <= 8) {
+        if (cmode) {
+          // count mode: keep only possible insertions, exact < T at P (float32
+          // exact sum of all K books, certified against hiT with K terms);
+          // candidate rows are read 8 at a time so their latencies overlap
+          Mask rest = cm;
+          while (rest) {
+            int idx[8];
+            Row rows[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              idx[u] = rest ? __ffsll((unsigned long long)rest) - 1 : -1;
+              if (idx[u] >= 0) {
+                rest &= rest - 1;
+                const int vv = idx[u] / IPC, jj = idx[u] % IPC;
+                rows[u] = load_row(p.codes_full, p.KP,
+                                   (int64_t)t + (lane * V + vv) * IPC + jj);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              if (idx[u] < 0) continue;
+              float e = 0.f;
+              for (int b2 = 0; b2 < K; ++b2) e += lut32k[b2 * m + (int)rows[u].byte(b2)];
+              if (!(e < hiT)) cm &= ~((Mask)1 << idx[u]);
             }
           }
         }
@@ -998,9 +1060,11 @@ __device__ __forceinline__ int replay_window(Live& L, const RCtx& c, int lane,
         const uint32_t imask = __ballot_sync(kFull, ins);
         const int first = imask ? __ffs(imask) - 1 : 31;
         const uint32_t decided = imask ? (kFull >> (31 - first)) : kFull;
-        L.refinements += __popc(rmask & decided);
+        if (!c.count_mode) {  // (count mode: the count kernel tallies refinements)
+          L.refinements += __popc(rmask & decided);
+          if (refined && ((decided >> lane) & 1u)) record_survivor(c.surv, id);
+        }
         L.candidates += __popc(rmask & decided);
-        if (refined && ((decided >> lane) & 1u)) record_survivor(c.surv, id);
         done |= decided;
         if (!imask) break;
         const double ne = __shfl_sync(kFull, e64, first);
@@ -1009,6 +1073,13 @@ __device__ __forceinline__ int replay_window(Live& L, const RCtx& c, int lane,
         L.H.replace_max(ne, nid, nf, lane);
         live_update64(L, c.sigma, c.k, c.f32);  // (the replay never uses the float32 bounds)
         ++L.insertions;
+        if (c.count_mode) {  // items after nid are refined against the new threshold
+          if (lane == 0) {
+            if (L.ntraj < kMaxTraj) c.traj[L.ntraj] = TrajEntry{(int64_t)nid, L.thr64};
+            else atomicOr(c.error, 16);
+          }
+          ++L.ntraj;
+        }
         if (L.thr64 > cap || L.thr64 <= floor_) {
           const int r = __shfl_sync(kFull, wpos, first);
           __syncwarp();
@@ -1123,6 +1194,10 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   c.pw = false;  // n >= 2 whenever the replay runs (P >= k >= 1 and P < n)
   c.wide = false;
   c.surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
+  c.count_mode = st.count_mode != 0;
+  c.traj = p.traj + (size_t)q * kMaxTraj;
+  c.error = p.error;
+  L.ntraj = st.ntraj;
   const double theta = st.thr;  // the lists' threshold
   const int64_t SW = p.RS / kFW;
 
@@ -1395,7 +1470,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           ent.w = (uint32_t)(fb >> 32);
           src[i] = ent;
           ex[i] = __longlong_as_double(0x7ff8000000000000LL);
-          if (f < thr && (int64_t)ent.x > skp && !(p.debug & 2))
+          if ((f < thr || c.count_mode) && (int64_t)ent.x > skp && !(p.debug & 2))
             plist[atomicAdd((int*)&ctl[2], 1)] = i;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kRP));
@@ -1452,6 +1527,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             uint2 tl[kWU];
             double exv[kWU];
             bool valid[kWU];
+            bool any = false;
 #pragma unroll
             for (int u = 0; u < kWU; ++u) {
               const int e = w0 + u * 32 + lane;
@@ -1460,9 +1536,16 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
               ids[u] = (int32_t)ent.x;
               tl[u] = make_uint2(ent.z, ent.w);  // float64 fast score (prep)
               exv[u] = valid[u] ? exs[e] : 0.0;
+              // count mode: only insertions matter; exact >= T now can never
+              // insert again (T never increases)
+              if (c.count_mode && valid[u] && exv[u] >= L.T64) valid[u] = false;
+              any |= valid[u];
             }
+            if (c.count_mode && !__any_sync(kFull, any)) continue;
+            // (count mode: the lists hold every possible insertion whatever the
+            // live threshold is -- no walks)
             const int b = replay_window<16>(L, c, lane, ids, tl, exv, valid, sid, sidx, sfv, sfe,
-                                            lutf, theta, -kInf64);
+                                            lutf, c.count_mode ? kInf64 : theta, -kInf64);
             if (b >= 0) {  // the live threshold rose above theta: walk from the next item
               const int32_t y = __shfl_sync(kFull, ids[b >> 5], b & 31);
               if (lane == 0) { *walk_from = (long long)y + 1; ctl[3] = 1; }
@@ -1482,7 +1565,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
             // words, 64k-item sub-ranges) and exact-score slot are free)
             walk(lo, hi_, false, reinterpret_cast<uint32_t*>(ring + (ch % kRSlots) * kCH),
                  reinterpret_cast<int32_t*>(ring_e + (ch % kRSlots) * kCH), kCH * 16 * 8);
-            if (warp == 0 && lane == 0 && L.thr64 > theta && hi_ < n && !ctl[16]) {
+            if (warp == 0 && lane == 0 && L.thr64 > theta && hi_ < n && !ctl[16] && !c.count_mode) {
               *walk_from = hi_;  // the lists stop covering the items after the slice
               ctl[3] = 1;
             }
@@ -1541,6 +1624,8 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       ns.ovf_pool = 0;
       ns.rounds = st.rounds + 1;
       ns.walked = st.walked + walked;
+      ns.ntraj = L.ntraj;
+      if (st.count_mode) ns.thr = st.thr;  // (still the valid stale bound: no walks)
       p.qs[q] = ns;
     }
     return;
@@ -1548,6 +1633,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   if (tid == 0) {
     p.qs[q].done = 1;
     p.qs[q].P = n;  // later filter rounds skip this query
+    p.qs[q].ntraj = L.ntraj;  // (count mode: the count kernel's segments)
   }
   // output: heap ascending by (score, id) (search.py:156-165)
   for (int i = tid; i < k; i += kRW * 32) {
@@ -1579,6 +1665,179 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   }
 }
 
+// ==========================================================================
+// K5: refinement count (count-mode queries)
+// ==========================================================================
+// For a count-mode query the replay decided only the possible insertions and
+// recorded the live threshold after each one (TrajEntry: items > pos use thr;
+// thr0 before the first).  Every item i >= P0 is refined iff
+// fast64(i) < thr(i) (search.py:149) -- a parallel test once the trajectory
+// is known.  This kernel streams the fast codes like the filter (coalesced
+// 16-byte tile loads, lane-private float32 LUT pages, certified float32 test
+// with a float64 decision in the uncertain band), counts the refined items
+// into refinements[q] and sets their survivor bits.
+template <int FP>
+__global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_constant__ PipeParams p) {
+  using G = FGeo<FP>;
+  constexpr int IPC = G::IPC, V = G::V, TILE = G::TILE, N = V * IPC;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t dyn_size;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_size));
+  if (smem_addr(dsm) != kDynBase || smem_addr(dsm) + dyn_size < G::kSmemEnd) {
+    if (tid == 0) atomicOr(p.error, 1);
+    return;
+  }
+  uint32_t Lp[FP];
+#pragma unroll
+  for (int s = 0; s < FP; ++s)
+    Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
+            (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
+  const int K = p.K, m = p.m, F = p.F;
+  const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
+  const int64_t U = (int64_t)p.Q * p.NR;
+  const bool rmaj = p.range_major != 0;
+  int64_t u0, u1, ustep;
+  if (rmaj) { u0 = blockIdx.x; u1 = U; ustep = gridDim.x; }
+  else { u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1; }
+  const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
+  double* lut64f = reinterpret_cast<double*>(dsm);
+  (void)K;
+  int cur_q = -1;
+  for (int64_t u = u0; u < u1; u += ustep) {
+    const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
+    const int r = rmaj ? (int)(u / p.Q) : (int)(u % p.NR);
+    if (!p.qs[q].count_mode) continue;  // (uniform per unit)
+    const int64_t P0 = p.qs[q].P0;
+    const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
+    if (P0 >= r_hi) continue;
+    if (q != cur_q) {
+      __syncthreads();
+      const double* glut = p.lut64 + (size_t)q * K * m;
+      for (int i = tid; i < FP * m; i += kFW * 32) {
+        const int s = i / m, j = i - s * m;
+        const float v = s < F ? __double2float_rn(glut[p.fast_books[s] * m + j]) : 0.f;
+        const uint32_t a0 = kPage * (1 + s / G::BPR) + j * 256 + (s % G::BPR) * 4 * G::R;
+#pragma unroll
+        for (int rr = 0; rr < G::R; rr += 4) sts_f32x4(a0 + rr * 4, v);
+      }
+      for (int i = tid; i < F * m; i += kFW * 32) {
+        const int s = i / m, j = i - s * m;
+        lut64f[i] = glut[p.fast_books[s] * m + j];
+      }
+      __syncthreads();
+      cur_q = q;
+    }
+    const TrajEntry* tr = p.traj + (size_t)q * kMaxTraj;
+    const int nt = min(p.qs[q].ntraj, kMaxTraj);
+    const double thr0 = p.qs[q].thr0;
+    uint32_t* surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
+    const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, n);
+    const int64_t start = max(w_lo, P0);
+    unsigned long long refined = 0;
+    // threshold of item i: the last trajectory entry with pos < i (binary search)
+    auto seg_of = [&](int64_t i) -> int {
+      int lo2 = 0, hi2 = nt;  // number of entries with pos < i
+      while (lo2 < hi2) {
+        const int mid = (lo2 + hi2) >> 1;
+        if (tr[mid].pos < i) lo2 = mid + 1; else hi2 = mid;
+      }
+      return lo2;
+    };
+    int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
+    int sg = seg_of(t);  // then advanced monotonically: each change point is crossed once
+    double thr = sg ? tr[sg - 1].thr : thr0;
+    int64_t next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
+    float lo, hi;
+    certified_bounds(thr, F, lo, hi);
+    uint4 a[V];  // the next tile's chunks (register double buffer)
+    if (t < w_hi) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + t / IPC + lane + v * 32);
+    }
+    for (; t < w_hi; t += TILE) {
+      uint4 x[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) x[v] = a[v];
+      if (t + TILE < w_hi) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + (t + TILE) / IPC + lane + v * 32);
+      }
+      // the tile's segment(s): one threshold unless a change point falls inside
+      if (next_pos < t) {
+        while (sg < nt && tr[sg].pos < t) ++sg;
+        thr = sg ? tr[sg - 1].thr : thr0;
+        next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
+        certified_bounds(thr, F, lo, hi);
+      }
+      const bool split = next_pos < t + TILE - 1;
+      const bool full = t >= start && t + TILE <= w_hi;
+      const int64_t i0 = t + (int64_t)lane * N;
+      // fast sums of the lane's N items (lane-private gathers, as the filter)
+      float fv[N];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+#pragma unroll
+        for (int j = 0; j < IPC; ++j) {
+          float f = 0.f;
+#pragma unroll
+          for (int s2 = 0; s2 < FP; ++s2) {
+            const int byte = j * FP + s2;
+            const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
+            f += lds_f32(__byte_perm(wd[byte >> 2], Lp[s2], sel));
+          }
+          fv[v * IPC + j] = f;
+        }
+      }
+      unsigned long long bits = 0, band = 0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        bits |= (fv[j] < lo) ? (1ull << j) : 0ull;
+        band |= (fv[j] < hi) ? (1ull << j) : 0ull;
+      }
+      band &= ~bits;  // float32 cannot decide these: float64 below
+      if (!full || split || __any_sync(kFull, band != 0)) {
+        // (rare) edge tiles, a threshold change inside the tile, near-ties
+        bits = 0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+#pragma unroll
+          for (int j = 0; j < IPC; ++j) {
+            const int64_t i = i0 + v * IPC + j;
+            if (i < start || i >= w_hi) continue;
+            double th = thr;
+            float l2 = lo, h2 = hi;
+            if (split) {
+              const int s3 = seg_of(i);
+              th = s3 ? tr[s3 - 1].thr : thr0;
+              certified_bounds(th, F, l2, h2);
+            }
+            const float f = fv[v * IPC + j];
+            bool ref = f < l2;
+            if (!ref && f < h2) ref = tuple_f64<FP>(chunk_tuple<FP>(x[v], j), lut64f, m, F) < th;
+            if (ref) bits |= 1ull << (v * IPC + j);
+          }
+        }
+      }
+      refined += (unsigned long long)__popcll(bits);
+      if (surv && bits) {  // this lane's items are one contiguous, N-aligned run
+        constexpr int W = N >= 32 ? N / 32 : 1;
+#pragma unroll
+        for (int h = 0; h < W; ++h) {
+          const uint32_t wv = N >= 32 ? (uint32_t)(bits >> (32 * h))
+                                      : (uint32_t)bits << (int)((i0 & 31));
+          if (wv) atomicOr(surv + ((i0 + 32 * h) >> 5), wv);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) refined += __shfl_xor_sync(kFull, refined, o);
+    if (lane == 0 && refined && p.refinements)
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.refinements + q), refined);
+  }
+}
+
 // --------------------------------------------------------------------------
 // host launch
 // --------------------------------------------------------------------------
@@ -1598,6 +1857,9 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
                                   (int)(kSmemWindow - kDynBase))) != cudaSuccess)
       return e;
     if ((e = cudaFuncSetAttribute(icq_filter_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(kSmemWindow - kDynBase))) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(icq_count_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kSmemWindow - kDynBase))) != cudaSuccess)
       return e;
     return cudaFuncSetAttribute(icq_replay_kernel<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1630,6 +1892,11 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     cudaEventRecord(ev[2 + 2 * r], s);
     cudaEventRecord(ev[3 + 2 * r], s);
   }
+  if (FP <= 8 && !p.exact_mode && p.count_used) {  // refinement count of count-mode queries
+    icq_count_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (ev) cudaEventRecord(ev[2 + 2 * kMaxRounds], s);
   return cudaSuccess;
 }
 

@@ -35,7 +35,13 @@ struct QState {
   int32_t wide;         // float32 certification off: float64 only
   int32_t done;         // all items decided, outputs written (later rounds skip it)
   int32_t rounds;       // filter/replay rounds before this one
-  int32_t pad_;
+  int32_t count_mode;   // refinement-heavy query: the lists hold only possible insertions
+                        // (fast < thr and exact < T at P); the replay records the threshold
+                        // trajectory and the count kernel tallies refinements / survivors
+  float hiT;            // count mode: certified float32 upper bound of T at P (K terms)
+  int32_t ntraj;        // count mode: insertions after P (trajectory entries)
+  double thr0;          // count mode: the live threshold at P0
+  int64_t P0;           // the prologue end (P moves when a walk hands a query to a new round)
   int64_t walked;       // items walked in order in earlier rounds
   int64_t skipped;      // items the filter did not stream (their slice overflowed:
                         // the replay rescans it from the codes)
@@ -49,7 +55,14 @@ constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
 constexpr int64_t kRangeAlign = 32768;
 constexpr int kMaxRounds = 4;  // filter/replay rounds per batch (walks past walk_cap resume)
-constexpr int kProfEvents = 2 + 2 * kMaxRounds;  // ranges / padding: whole filter tiles of every warp
+constexpr int kProfEvents = 3 + 2 * kMaxRounds;  // + the count kernel  // ranges / padding: whole filter tiles of every warp
+
+// count mode: the live threshold after an insertion at item pos (items > pos use thr)
+struct TrajEntry {
+  int64_t pos;
+  double thr;
+};
+constexpr int kMaxTraj = 8192;  // insertions after P per query in count mode
 
 struct PipeParams {
   const uint8_t* codes_fast;  // [n_pad * FP]   fast books only (row-major), zero padded
@@ -69,6 +82,8 @@ struct PipeParams {
   uint4* pool;                // [pool_pages * kPG] candidates {id, 0, fast-code tuple (FP <= 8) | f64 fast (FP = 16)}
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
+  TrajEntry* traj;            // [Q][kMaxTraj] count-mode threshold trajectories
+  unsigned long long* count_acc;  // [Q] count-mode refinements after P
   int64_t pool_pages;
   int64_t n;
   int64_t words;              // survivors bitmap words per query
@@ -85,6 +100,10 @@ struct PipeParams {
                               // max fast score over the J+1 largest-exact heap entries);
                               // -1: the loosest J on a ladder with a list share <= 1/list_div
   int32_t list_div;
+  int32_t count_div;          // count mode when the live threshold passes > 1/count_div of the
+                              // sampled items (0: never; ICQ_COUNT_MODE=1 forces it)
+  int32_t force_count;
+  int32_t count_used;         // count mode possible: launch the count kernel
   int32_t pro_live;           // prologue stop rule counts items under theta (1) or under M (0)
   int32_t sigma_f32;          // numpy promotion of a float32 sigma (see live_thr)
   int32_t rounds;             // filter/replay rounds (1..kMaxRounds)

@@ -194,8 +194,11 @@ class SearchIndex:
     cfg: Config = field(default_factory=Config)
 
     def __post_init__(self):
-        books = self.books if isinstance(self.books, CodebookSet) else CodebookSet(self.books)
-        codes = self.codes if isinstance(self.codes, CodeMatrix) else CodeMatrix(self.codes)
+        # (duck-typed: the reference's own CodebookSet / CodeMatrix are accepted too)
+        books = self.books if isinstance(self.books, CodebookSet) else CodebookSet(
+            getattr(self.books, "codewords", self.books))
+        codes = self.codes if isinstance(self.codes, CodeMatrix) else CodeMatrix(
+            getattr(self.codes, "codes", self.codes))
         self.books = CodebookSet(books.codewords.astype(np.float32, copy=False))
         self.codes = codes
         if codes.K != books.K:

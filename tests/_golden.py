@@ -5,7 +5,7 @@ from pathlib import Path
 import numpy as np
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-CASES = sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "eval_cli")
+CASES = sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem not in ("eval_cli", "encode_cases"))
 
 
 class Row:

@@ -104,6 +104,9 @@ CONFIGS = [
 #   rounds    - as filter, every walk past 1 item stops the query; the next
 #               filter/replay round lists its rest (4 rounds, the last unbounded)
 #   oneround  - as filter, a single round (walks run to completion)
+#   countmode - as filter, every query in count mode (the lists hold only
+#               possible insertions; the count kernel tallies refinements
+#               and survivor bits from the replay's threshold trajectory)
 _F = {"ICQ_PRO_MAX": "2048", "ICQ_PRO_MIN": "0"}
 MODES = {
     "default": {},
@@ -122,6 +125,10 @@ MODES = {
     # walks longer than 1 item hand the query to the next filter/replay round
     "rounds": dict(_F, ICQ_WALK_CAP="1", ICQ_ROUNDS="4"),
     "oneround": dict(_F, ICQ_ROUNDS="1"),
+    # refinement-heavy path forced on every query: lists of possible
+    # insertions only, refinements / survivors from the count kernel
+    "countmode": dict(_F, ICQ_COUNT_MODE="1"),
+    "countmode_overflow": dict(_F, ICQ_COUNT_MODE="1", ICQ_POOL_PAGES="2"),
 }
 
 

@@ -53,7 +53,7 @@ def test_shape_golden_batched(name):
 
 
 @pytest.mark.parametrize("mode", ["filter", "listj", "prolive", "overflow", "rangemajor",
-                                  "noties"])
+                                  "noties", "countmode"])
 @pytest.mark.parametrize("name", ["shape_c2", "shape_c3", "shape_c4", "shape_c5",
                                   "shape_c1_sigma_f32"])
 def test_shape_survivors_all_modes(name, mode, monkeypatch):
@@ -93,6 +93,8 @@ def _grown(c, n, seed):
     ("shape_c4", {"ICQ_RANGE_MAJOR": "1"}),
     ("shape_c4", {"ICQ_LIST_J": "8", "ICQ_PRO_MAX": "8192", "ICQ_PRO_MIN": "0"}),
     ("shape_c2", {"ICQ_PRO_LIVE": "1"}),
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_RANGE_MAJOR": "1"}),
+    ("shape_c4", {"ICQ_COUNT_MODE": "1"}),
 ])
 def test_two_million_vs_oracle(name, knobs, monkeypatch):
     for key, val in knobs.items():

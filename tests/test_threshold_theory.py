@@ -14,7 +14,7 @@ For every item i refined by the reference (fast_i < bound_i + sigma):
 import numpy as np
 import pytest
 
-from tools.sim_filter import replay
+from _threshold_sim import replay
 
 
 def _case(seed, n, K, F, m, dup):
@@ -77,3 +77,21 @@ def test_stale_thresholds_cover_refined_items(seed, sigma):
                     ins_between = int(((pos > p0) & (pos < i)).sum())
                     if ins_between <= J:
                         assert fast[i] < AJ, (seed, J, i)
+
+
+@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("sigma", [0.0, 1.0, 25.0, 1e9])
+def test_count_mode_candidates_cover_insertions(seed, sigma):
+    """Count mode lists only possible insertions: an item inserted after state
+    s has exact < T_s and therefore fast < T_s - Smin (slow part >= Smin) --
+    whatever sigma is (icq_pipeline.cuh prologue hand-off, count mode)."""
+    n, K, F, m, k = 1500, 6, 2, 8, 10
+    fast, exact, smin = _case(seed, n, K, F, m, dup=seed % 3 == 0)
+    _, states = _trajectory(fast, exact, k, sigma)
+    inserted = [s[0] for s in states[1:]]
+    for p0, heap in states:
+        T = heap[0][0]
+        for i in inserted:
+            if i > p0:
+                assert exact[i] < T
+                assert fast[i] < T - smin + 1e-9 * abs(T)

@@ -10,11 +10,9 @@ and recorded in every bench line:
 
 Codebooks are trained by the reference (tools/train_books.py, run in the build
 container) and committed under bench_data/.  The database is encoded on the
-GPU by ``encode_icm`` — a torch restatement of the reference encoder
-``assign_codes`` (train.py:196-243: greedy residual build-up, then ICM sweeps
-that re-pick one book's code with the others fixed, strict improvement only),
-used here only to prepare bench data (the native CUDA encoder is the next
-scope row).  fp32 matmuls (TF32 off) in place of the reference's fp64 BLAS.
+GPU by the package's float64 ICM encoder (paper_1912_08756_b200.encode_device,
+icq_encode.cu: the reference's assign_codes, train.py:196-243, pinned to it
+by tests/test_gpu_encode.py), chunk by chunk as it is generated.
 """
 
 from __future__ import annotations
@@ -105,60 +103,31 @@ def load_books(w: Workload):
     return z["books"].astype(np.float32), meta
 
 
-def encode_icm(x, books, sweeps: int = 10, chunk: int = 1 << 21):
-    """(n, d) float32 cuda tensor -> (n, K) uint8 codes (greedy + ICM, train.py:196-243)."""
+def build_database(w: Workload, books, sweeps: int = 10, chunk_rows: int = 1 << 22,
+                   device="cuda", stats: dict | None = None):
+    """Generate the config's database chunk by chunk on the GPU, encode it with
+    the float64 ICM encoder, and keep only the uint8 codes (n, K) on the device."""
+    import time
+
     import torch
 
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        B = torch.as_tensor(books, device=x.device, dtype=torch.float32)  # (K, m, d)
-        K, m, _ = B.shape
-        c_sq = (B * B).sum(-1)  # (K, m)
-        out = torch.empty((x.shape[0], K), dtype=torch.uint8, device=x.device)
-        for s in range(0, x.shape[0], chunk):
-            xs = x[s:s + chunk]
-            rows = torch.arange(xs.shape[0], device=x.device)
-            codes = torch.empty((xs.shape[0], K), dtype=torch.int64, device=x.device)
-            res = xs.clone()
-            for b in range(K):
-                dist = c_sq[b][None, :] - 2.0 * (res @ B[b].T)
-                codes[:, b] = dist.argmin(1)
-                res -= B[b][codes[:, b]]
-            recon = xs - res
-            for _ in range(sweeps):
-                changed = 0
-                for b in range(K):
-                    cur = codes[:, b]
-                    target = xs - (recon - B[b][cur])
-                    dist = c_sq[b][None, :] - 2.0 * (target @ B[b].T)
-                    best = dist.argmin(1)
-                    imp = dist[rows, best] < dist[rows, cur]
-                    hit = imp.nonzero().squeeze(1)
-                    if hit.numel():
-                        recon[hit] += B[b][best[hit]] - B[b][cur[hit]]
-                        codes[hit, b] = best[hit]
-                        changed += hit.numel()
-                if changed == 0:
-                    break
-            out[s:s + chunk] = codes.to(torch.uint8)
-        return out
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
-
-
-def build_database(w: Workload, books, sweeps: int = 4, chunk_rows: int = 1 << 22,
-                   device="cuda"):
-    """Generate the config's database chunk by chunk on the GPU, encode it, and
-    keep only the uint8 codes (n, K) on the device."""
-    import torch
+    from paper_1912_08756_b200.encode import encode_device
 
     codes = torch.empty((w.n, w.K), dtype=torch.uint8, device=device)
+    used, t_enc = 0, 0.0
     for ci, s in enumerate(range(0, w.n, chunk_rows)):
         e = min(w.n, s + chunk_rows)
-        x = sample_torch(w, e - s, SEED_DB + ci, device)
-        codes[s:e] = encode_icm(x, books, sweeps=sweeps)
-        del x
+        x = sample_torch(w, e - s, SEED_DB + ci, device).float()
+        torch.cuda.synchronize()
+        t0 = time.time()
+        c, u = encode_device(x, books, max_sweeps=sweeps)
+        torch.cuda.synchronize()
+        t_enc += time.time() - t0
+        codes[s:e] = c
+        used = max(used, u)
+        del x, c
+    if stats is not None:
+        stats.update(encode_seconds=t_enc, sweeps_used=used, max_sweeps=sweeps)
     return codes
 
 
