@@ -476,6 +476,8 @@ def sigma_sweep(args, w, dev, meta, sigma0, batch, flush, stream, ex, Qall):
     pts = [("mean_lambda", lam), ("4_mean_lambda", 4 * lam)]
     if learned not in (0.0, sigma0, lam, 4 * lam):
         pts.append(("learned", learned))
+    if sigma0 != 0.0:
+        pts.insert(0, ("zero", 0.0))
     ei = ex["ids"].cpu().numpy()
     out = []
     for label, sg in pts:

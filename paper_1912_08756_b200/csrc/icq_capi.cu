@@ -425,7 +425,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   p.pro_live = (int32_t)env_i("ICQ_PRO_LIVE", 0);
   // count mode (refinement-heavy queries: the live threshold passes > 1/count_div
   // of the sampled items): lists of possible insertions + a parallel count
-  p.count_div = exact ? 0 : (int32_t)env_i("ICQ_COUNT_DIV", 128);
+  p.count_div = exact ? 0 : (int32_t)env_i("ICQ_COUNT_DIV", 256);
   p.force_count = exact ? 0 : (int32_t)env_i("ICQ_COUNT_MODE", 0);
   p.count_used = (FP <= 8 && (p.count_div > 0 || p.force_count)) ? 1 : 0;
   {

@@ -48,6 +48,31 @@ __device__ __forceinline__ Row load_row(const uint8_t* codes_full, int KP, int64
   return r;
 }
 
+// Same, with an L2 evict_last policy: count-mode candidate rows are re-read
+// by every query of a batch scanning the same range; keep them resident
+// against the fast-code stream.
+__device__ __forceinline__ Row load_row_keep(const uint8_t* codes_full, int KP, int64_t id,
+                                             uint64_t pol) {
+  Row r;
+  r.w[0] = r.w[1] = r.w[2] = r.w[3] = 0;
+  const uint8_t* p = codes_full + id * KP;
+  if (KP == 16) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]) : "l"(p), "l"(pol));
+  } else if (KP == 8) {
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(r.w[0]), "=r"(r.w[1]) : "l"(p), "l"(pol));
+  } else {
+    return load_row(codes_full, KP, id);
+  }
+  return r;
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // Tile-transposed layout of the streamed fast rows (codes_fast): within each
 // tile of 128 16-byte chunks, logical chunk lc = 4*lane + v is stored at
 // physical chunk 32*v + lane.  A coalesced warp load of chunks 32*v + lane

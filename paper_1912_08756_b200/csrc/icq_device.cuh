@@ -13,10 +13,6 @@
 namespace icq {
 
 constexpr int kMaxK = 16;          // books per index supported by this build
-constexpr int kNS = 8;             // scan warps per CTA (warp 0 is the replay warp)
-constexpr int kThreads = (kNS + 1) * 32;
-constexpr int kNC = kNS * 64;      // 16-byte code chunks ("groups") per segment
-constexpr int kValStride = kNC + 1;  // padded row stride of the slot value table
 constexpr uint32_t kPage = 65536;  // lane-private LUT pages live at 64 KiB-aligned smem addresses
 constexpr uint32_t kSmemWindow = 233472;  // B200: 1 KiB reserved + 227 KiB dynamic
 constexpr uint32_t kDynBase = 1024;       // dynamic smem base when the kernel has no static smem
@@ -38,32 +34,6 @@ __device__ __forceinline__ void sts_f32x4(uint32_t a, float v) {  // v in 4 cons
 }
 __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
-
-// --------------------------------------------------------------------------
-// mbarrier (CTA scope) — producer/consumer hand-off between scan warps and
-// the replay warp.
-// --------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-// Arrive on `a` when all of this thread's prior cp.async copies have landed
-// (pending count +1 now, -1 asynchronously: net zero, the phase also waits on
-// the copies).
-__device__ __forceinline__ void mbar_arrive_cp_async(uint32_t a) {
-  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(a),
-      "r"(parity)
-      : "memory");
 }
 
 // bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2

@@ -1,4 +1,4 @@
-// icq_pipeline.cuh — the ICQ two-step query path as three kernels per batch.
+// icq_pipeline.cuh — the ICQ two-step query path as kernels per batch.
 // (templates; instantiated per fast-row width in icq_pipe_fp*.cu, dispatched
 // by icq_pipeline.cu)
 //
@@ -7,29 +7,28 @@
 // sigma = 0: then fast == exact and the prune predicate is the top-k test).
 //
 // The reference walks the database in order with a heap whose FAST score of
-// the maximum is the pruning bound (:149).  That chain is sequential, but the
-// bound is dominated by a monotone stale threshold (see
-// stale_filter): once the heap has settled, one threshold is valid for
-// every later item, so the streaming part can run on all SMs at once and
-// only the few items below it need the in-order replay.
+// the maximum is the pruning bound (:149).  The chain is sequential, but
+// thresholds that dominate the live one let the streaming run on all SMs
+// (tests/test_threshold_theory.py):
 //
 //   K2 icq_prologue_kernel  one CTA per query: the insertion-heavy start of
-//        the database, in order, until a block passes <= 1/pro_div of its
-//        items under the stale threshold.  fp32 prefilter (non-replicated
-//        table), float64 scores of the prefiltered items, warp-0 decisions in
-//        float64.  Leaves the heap, the refinement count and the fp32
-//        filter threshold `hi` for the rest.
+//        the database, in order (stale-threshold fp32 prefilter, float64
+//        scores, warp-0 ballot-window decisions).  Ends with the list
+//        threshold theta = A_J + sigma (J from a sampled ladder) or, for
+//        refinement-heavy queries, count mode.
 //   K3 icq_filter_kernel    the hot path: every SM streams fast-code bytes
-//        (16-byte loads, register double buffer + L2 bulk prefetch), gathers
-//        |F| fp32 entries per item from lane-private replicated LUT pages
-//        (one byte_perm per lookup, bank-conflict free) and compacts items
-//        with x32 < hi, in item order, into per-(query, range, warp) slices
-//        of a paged candidate pool.  No sequential dependency at all.
-//   K4 icq_replay_kernel    one warp per query: resumes the reference loop at
-//        the prologue end over the candidate slices in database order
-//        against the LIVE bound (certified fp32 test, float64 for the items
-//        it refines), heap insertions, output sorted by (score, id).  A slice
-//        whose candidates overflowed its pages is rescanned from the codes.
+//        (16-byte loads, register double buffer), gathers |F| fp32 entries
+//        per item from lane-private replicated LUT pages (one byte_perm per
+//        lookup, bank-conflict free) and compacts items under theta, in item
+//        order, into per-(query, range, warp) slices of a paged pool
+//        (count mode: only items that can still be inserted).
+//   K4 icq_replay_kernel    one CTA per query: resumes the reference loop at
+//        the prologue end over the slices in database order against the LIVE
+//        bound; walks the database in order while the live threshold is
+//        above theta; long walks hand the query to the next round.  Count
+//        mode: insertions only, recording the threshold trajectory.
+//   K5 icq_count_kernel     count mode: refinement counts and survivor bits
+//        of every item against the trajectory, streamed like K3.
 //
 // Every decision compares the reference's float64 values, so ids, scores,
 // refinement counts and survivor sets are bitwise the reference's.
@@ -702,6 +701,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
     const bool cmode = FP <= 8 && p.qs[q].count_mode != 0;
+    const uint64_t keep_pol = l2_evict_last_policy();
     const float hiT = p.qs[q].hiT;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
@@ -893,8 +893,8 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
               if (idx[u] >= 0) {
                 rest &= rest - 1;
                 const int vv = idx[u] / IPC, jj = idx[u] % IPC;
-                rows[u] = load_row(p.codes_full, p.KP,
-                                   (int64_t)t + (lane * V + vv) * IPC + jj);
+                rows[u] = load_row_keep(p.codes_full, p.KP,
+                                        (int64_t)t + (lane * V + vv) * IPC + jj, keep_pol);
               }
             }
 #pragma unroll
