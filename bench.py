@@ -65,9 +65,12 @@ def _profiled_traffic(cfg: str):
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons during the timed region,
-    sampled in-process through NVML every 20 ms.  (An `nvidia-smi -lms 20`
-    child, the first version, stalled the launch path for 5-70 ms in about
-    half of the c4 runs; NVML clock queries measured clean.)"""
+    sampled in-process through NVML every 250 ms, plus one sample taken while
+    the last steps still run.  (An `nvidia-smi -lms 20` child, the first
+    version, stalled the launch path for 5-70 ms in about half of the c4
+    runs; in-process NVML queries every 20 ms still cost the long c5 kernels
+    ~6-18 % -- 91-103 ms per step against 86 ms without the sampler -- so the
+    sampler now runs at 4 Hz.)"""
 
     NAMES = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
              ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
@@ -118,7 +121,7 @@ class ClockSampler:
             self._first.set()
             if self.recording:
                 self.rows.append((float(sm), float(self._mx), int(rb)))
-            self._stop.wait(0.02)
+            self._stop.wait(0.25)
 
     def sample_now(self):
         """One sample from the calling thread (short timed regions: taken
@@ -147,7 +150,7 @@ class ClockSampler:
         reasons = sorted({nm for r in self.rows for nm, bit in self.NAMES if r[2] & bit})
         return {"sm_mhz": float(np.median([r[0] for r in self.rows])),
                 "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
-                "samples": len(self.rows), "source": "NVML, 20 ms"}
+                "samples": len(self.rows), "source": "NVML, 250 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -302,10 +305,10 @@ def main():
     L.icq_profile_enable(0)
     import ctypes as _C
 
-    kms = (_C.c_double * 4)()
+    kms = (_C.c_double * 5)()
     klaunch = _C.c_int32()
     L.icq_profile_read(kms, _C.byref(klaunch))
-    t_pro_k, t_filter_k, t_replay_k, t_count_k = (x / 1e3 for x in kms)
+    t_pro_k, t_filter_k, t_replay_k, t_count_k, t_refine_k = (x / 1e3 for x in kms)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -430,6 +433,8 @@ def main():
                     "wide_queries": int((stats[:, 7].long() & 0xFF).sum().item()),
                     "prologue_f64_scored_per_query": float(stats[:, 8].mean().item()),
                     "filter_candidates_per_query": float(stats[:, 9].mean().item()),
+                    "refine_inputs_per_query": float(stats[:, 11].mean().item()),
+                    "refine_inputs_max_query": float(stats[:, 11].max().item()),
                     "filter_skipped_items_per_query": float(stats[:, 15].mean().item()),
                     "filter_pass_fraction": float(stats[:, 9].mean().item() / w.n),
                     "prologue_phase_cycles_per_query": {
@@ -448,6 +453,7 @@ def main():
         "kernels_ms_per_step": {"lut": t_lut / args.steps * 1e3,
                                 "prologue": t_pro_k / args.steps * 1e3,
                                 "filter": t_filter_k / args.steps * 1e3,
+                                "refine": t_refine_k / args.steps * 1e3,
                                 "replay": t_replay_k / args.steps * 1e3,
                                 "count": t_count_k / args.steps * 1e3},
         "clocks": clk.summary(),

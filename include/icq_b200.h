@@ -173,8 +173,8 @@ icq_status icq_workspace_size(icq_index_t h, int32_t Q, int32_t k, size_t* bytes
  *                  items decided by the replay, items walked in order, prologue end,
  *                  prologue / replay cycles, rescanned slices (| overflow
  *                  counts << 20 / << 40), wide flag, prologue float64 scorings,
- *                  filter candidates, prologue insertions, filter threshold
- *                  (float32 bits), prologue phase cycles
+ *                  filter candidates, prologue insertions, count-mode entries
+ *                  listed before the refine kernel, prologue phase cycles
  *   fallback_out : optional host int32; set to 1 when the fast set is empty and
  *                  the exact engine ran instead (search.py:127-131)
  * Kernels run on `stream`; the call synchronizes it once at the end and
@@ -217,11 +217,11 @@ icq_status icq_search_host(icq_index_t h, const double* q_host, int32_t Q, int32
 /* ---------------------------------------------------------------------------
  * Instrumentation (bench / profiling only; not part of the reference surface).
  * icq_profile_enable(1) makes every following search call record CUDA events
- * on its launch stream around the kernels of each batch (prologue, filter
- * and replay of every round, refinement count).  icq_profile_read
+ * on its launch stream around the kernels of each batch (prologue; filter,
+ * refine and replay of every round; refinement count).  icq_profile_read
  * synchronizes those events and returns the summed device milliseconds per
- * kernel kind (ms_out[4]: prologue, filter, replay, count) and the number of
- * batches recorded, then clears the record.
+ * kernel kind (ms_out[5]: prologue, filter, replay, count, refine) and the
+ * number of batches recorded, then clears the record.
  * ------------------------------------------------------------------------- */
 icq_status icq_profile_enable(int32_t on);
 icq_status icq_profile_read(double* ms_out, int32_t* launches);

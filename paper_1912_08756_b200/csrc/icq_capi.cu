@@ -4,6 +4,7 @@
 // (build_lut :61, search_exact :97, search_two_step :112) and the argument
 // layout of icq.data.SearchIndex (data.py:193-263).  Validation mirrors
 // search.py:47-58, :123-131 and data.py:145-176.
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdlib>
@@ -220,7 +221,7 @@ icq_status icq_profile_enable(int32_t on) {
 
 icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   std::lock_guard<std::mutex> g(g_prof_mu);
-  double acc[4] = {0, 0, 0, 0};  // prologue, filter, replay, count
+  double acc[5] = {0, 0, 0, 0, 0};  // prologue, filter, replay, count, refine
   const int groups = (int)(g_prof_events.size() / kProfEvents);
   for (int i = 0; i < groups; ++i) {
     cudaEvent_t* e = &g_prof_events[kProfEvents * i];
@@ -229,12 +230,14 @@ icq_status icq_profile_read(double* ms_out, int32_t* launches) {
     for (int j = 0; j + 1 < kProfEvents; ++j) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, e[j], e[j + 1]);
-      acc[j == 0 ? 0 : (j == kProfEvents - 2 ? 3 : (j % 2 == 1 ? 1 : 2))] += ms;
+      // interval j: 0 prologue; 1 + 3r filter, 2 + 3r refine, 3 + 3r replay; last count
+      static const int kind3[3] = {1, 4, 2};
+      acc[j == 0 ? 0 : (j == kProfEvents - 2 ? 3 : kind3[(j - 1) % 3])] += ms;
     }
   }
   for (cudaEvent_t e : g_prof_events) cudaEventDestroy(e);
   g_prof_events.clear();
-  if (ms_out) for (int j = 0; j < 4; ++j) ms_out[j] = acc[j];
+  if (ms_out) for (int j = 0; j < 5; ++j) ms_out[j] = acc[j];
   if (launches) *launches = groups;
   return ICQ_OK;
 }
@@ -408,7 +411,10 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     // overflows a slice's kMaxPages * kPG candidates
     int64_t cap = h->n / 16;
     if (cap < ((int64_t)1 << 18)) cap = (int64_t)1 << 18;
-    if (big) cap = (int64_t)4 << 20;
+    // (streams larger than L2: 1M-item ranges keep a range's fast codes and
+    // candidate rows L2-resident while every query of the batch sweeps it, and
+    // a 64k-item slice holds up to 25 % of its items as candidates)
+    if (big) cap = (int64_t)1 << 20;
     if (rs > cap) rs = cap;
     rs = env_i("ICQ_RANGE_ITEMS", rs);
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
@@ -427,6 +433,9 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   // of the sampled items): lists of possible insertions + a parallel count
   p.count_div = exact ? 0 : (int32_t)env_i("ICQ_COUNT_DIV", 256);
   p.force_count = exact ? 0 : (int32_t)env_i("ICQ_COUNT_MODE", 0);
+  // ... and only when those lists would be long: a replay CTA decides short
+  // lists faster than the count pass streams the database once more
+  p.count_min = env_i("ICQ_COUNT_MIN", (int64_t)1 << 18);
   p.count_used = (FP <= 8 && (p.count_div > 0 || p.force_count)) ? 1 : 0;
   {
     const int64_t r = env_i("ICQ_ROUNDS", kMaxRounds);
@@ -452,7 +461,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     // is sized generously -- HBM is plentiful, the pool is never cleared
     // (only its top counter)
     int64_t entries = (int64_t)Qb * h->n / 8;
-    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 30;  // <= 16 GiB
+    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 31;  // <= 32 GiB
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
     p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
   }
@@ -475,9 +484,16 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   const size_t b_top = 256;  // pool_top, error word
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
   const size_t b_tr = p.count_used ? al((size_t)Qb * kMaxTraj * sizeof(TrajEntry)) : 0;
-  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl + b_tr;
+  const size_t b_cm = al(sizeof(int32_t) * (1 + (size_t)Qb));
+  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl + b_tr + b_cm;
   char* sc = nullptr;
+  const bool trace = (p.debug & 32) != 0;  // host-side timing of this call (stderr)
+  const auto tr0 = std::chrono::steady_clock::now();
+  auto tr_ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
+  };
   CUDA_TRY(cudaMallocAsync((void**)&sc, scratch, s));
+  const double tr_alloc = tr_ms();
   {
     char* o = sc;
     p.qs = reinterpret_cast<QState*>(o); o += b_qs;
@@ -490,6 +506,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     o += b_top;
     p.slices = reinterpret_cast<int32_t*>(o); o += b_sl;
     p.traj = b_tr ? reinterpret_cast<TrajEntry*>(o) : nullptr;
+    o += b_tr;
+    p.cm_list = reinterpret_cast<int32_t*>(o);
   }
   (void)b_lut;
   icq_status st = ICQ_OK;
@@ -511,6 +529,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     b.survivors = (!exact && survivors) ? survivors + (size_t)q0 * p.words : nullptr;
     b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
     e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.cm_list, 0, sizeof(int32_t), s);
     int unsupported = 0;
     cudaEvent_t* ev = nullptr;
     cudaEvent_t evs[kProfEvents];
@@ -535,9 +554,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     e = cudaMemcpyAsync(herr, p.error, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) st = fail(ICQ_ERR_CUDA, "search: %s", cudaGetErrorString(e));
   }
+  const double tr_launch = tr_ms();
   cudaFreeAsync(sc, s);
+  const double tr_free = tr_ms();
   if (st != ICQ_OK) return st;
   CUDA_TRY(cudaStreamSynchronize(s));
+  if (trace)
+    fprintf(stderr, "[icq trace] scratch %.1f MiB: alloc %.3f ms, launches done %.3f, free %.3f, sync %.3f\n",
+            scratch / 1048576.0, tr_alloc, tr_launch, tr_free, tr_ms());
   return check_call_errors(*herr);
 }
 

@@ -131,7 +131,7 @@ struct RepLayout {
   uint32_t lut64, lutf, he, hf, hi, wid, widx, wfv, wfe, meta, cum, chunks, ring, ringe, plist, ctl,
       total;
 };
-constexpr int kSG = 32;    // slices whose meta the replay stages in shared memory at once
+constexpr int kSG = 16;    // slices whose meta the replay stages in shared memory at once
 constexpr int kCH = 512;   // candidate entries per staged chunk (replay ring slot)
 constexpr int kRSlots = 4;  // replay ring: decide c | prepare c+1 | in flight c+2, c+3
 __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
@@ -562,7 +562,8 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     listJ = min(listJ, k - 1);
     // refinement-heavy: even the live threshold passes > 1/count_div of the
     // sample -> the lists would hold the refined items themselves
-    if (FP <= 8 && p.count_div > 0 && S > 0 && (int64_t)lad_cnt[0] * p.count_div > S)
+    if (FP <= 8 && p.count_div > 0 && S > 0 && (int64_t)lad_cnt[0] * p.count_div > S &&
+        (double)lad_cnt[0] * (double)(n - pos) > (double)p.count_min * (double)S)
       count_mode = true;
     __syncthreads();
   }
@@ -571,12 +572,14 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     const double A = heap_AJ(hf, k, listJ, lane, &best);
     double thr = wide ? kInf64 : thr_cover(A, p.sigma, f32s, false);
     float hiT = kInf;
+    double smin_cm = 0.0;
     if (count_mode) {
       // the lists keep every possible insertion, whatever sigma: an item
       // inserted later has exact < T_P (T never increases), hence
       // fast < T_P - Smin (its slow part is >= Smin); float64 slack for the
       // different summation orders of fast and exact scores
       const double sm = smin_rd(lut, K, m, p.fast_books, F, lane);
+      smin_cm = sm;
       const double T = he[0];
       thr = __dadd_ru(__dsub_ru(T, sm), fabs(T) * 1e-12);
       float loT;
@@ -617,13 +620,16 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       st.walked = 0;
       st.count_mode = count_mode ? 1 : 0;
       st.hiT = hiT;
+      st.smin = smin_cm;
       st.ntraj = 0;
       st.thr0 = live_thr(hf[0], hi[0], p.sigma, k, f32s);
       st.P0 = pos;
       st.ovf_pages = 0;
       st.ovf_pool = 0;
       st.skipped = 0;
+      st.listed_raw = 0;
       p.qs[q] = st;
+      if (count_mode) p.cm_list[1 + atomicAdd(p.cm_list, 1)] = q;
     }
   }
   for (int i = tid; i < k; i += kProThreads) {
@@ -685,8 +691,6 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
-  // count mode: float32 table of every book ([K][m], after lut64f, below the first page)
-  float* lut32k = reinterpret_cast<float*>(dsm + al16((uint32_t)(FP <= 8 ? FP : 8) * 256 * 8));
   const uint32_t two = 2u + (uint32_t)(p.n < 0);    // 2, opaque to the compiler (keeps IMADs)
   const uint32_t lt_mask = (1u << lane) - 1u;
   int cur_q = -1;
@@ -700,9 +704,6 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const uint2 mtup = make_uint2(p.qs[q].mtup[0], p.qs[q].mtup[1]);
     const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
-    const bool cmode = FP <= 8 && p.qs[q].count_mode != 0;
-    const uint64_t keep_pol = l2_evict_last_policy();
-    const float hiT = p.qs[q].hiT;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
     if (P >= r_hi || p.qs[q].done) {  // decided by the prologue / an earlier round
@@ -729,8 +730,6 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
         const int s = i / m, j = i - s * m;
         lut64f[i] = glut[p.fast_books[s] * m + j];
       }
-      if (FP <= 8 && p.qs[q].count_mode)
-        for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
       __syncthreads();
       cur_q = q;
     }
@@ -878,35 +877,6 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           }
         }
       }
-      if constexpr (FP <= 8) {
-        if (cmode) {
-          // count mode: keep only possible insertions, exact < T at P (float32
-          // exact sum of all K books, certified against hiT with K terms);
-          // candidate rows are read 8 at a time so their latencies overlap
-          Mask rest = cm;
-          while (rest) {
-            int idx[8];
-            Row rows[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              idx[u] = rest ? __ffsll((unsigned long long)rest) - 1 : -1;
-              if (idx[u] >= 0) {
-                rest &= rest - 1;
-                const int vv = idx[u] / IPC, jj = idx[u] % IPC;
-                rows[u] = load_row_keep(p.codes_full, p.KP,
-                                        (int64_t)t + (lane * V + vv) * IPC + jj, keep_pol);
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              if (idx[u] < 0) continue;
-              float e = 0.f;
-              for (int b2 = 0; b2 < K; ++b2) e += lut32k[b2 * m + (int)rows[u].byte(b2)];
-              if (!(e < hiT)) cm &= ~((Mask)1 << idx[u]);
-            }
-          }
-        }
-      }
       // positions: item order is (lane, v, j) -> an exclusive scan of the
       // per-lane counts; one ballot when no lane holds two
       const int mine = __popcll((unsigned long long)cm);
@@ -979,6 +949,95 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       cnt += T;
     }
     if (lane == 0) slice[0] = overflow ? -1 : cnt;
+  }
+}
+
+// ==========================================================================
+// K3b: refine (count-mode queries)
+// ==========================================================================
+// The filter lists, for a count-mode query, every item with
+// fast < T_P - Smin.  Only items with exact < T_P can ever be inserted (T
+// never increases), so this kernel rescores the listed items with the full
+// K-book table -- float32, certified against hiT with K terms: exact64 < T_P
+// implies e32 < hiT -- and compacts each slice in place, in order.  One CTA
+// per (query, range) with one warp per slice; units are range-major so the
+// CTAs in flight read candidate rows of the same range from L2.  Thousands of
+// warps each keep a page of row reads in flight: the random 8/16-byte row
+// reads that stalled the streaming kernel run at memory-system throughput.
+template <int FP>
+__global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_constant__ PipeParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  float* lut32k = reinterpret_cast<float*>(dsm);  // [K][m]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  if (!p.qs[q].count_mode || p.qs[q].done) return;  // (CTA-uniform)
+  const int64_t r_hi = min(p.n, ((int64_t)r + 1) * p.RS);
+  if (p.qs[q].P >= r_hi) return;
+  const int K = p.K, m = p.m, KP = p.KP;
+  const double* glut = p.lut64 + (size_t)q * K * m;
+  for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
+  __syncthreads();
+  int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+  const int cnt = slice[0];
+  if (cnt <= 0) return;  // empty, or overflowed (the replay walks it)
+  const float hiT = p.qs[q].hiT;
+  static_assert(kMaxPages <= 128, "page ids of a slice are held by 4 registers per lane");
+  int32_t pg[(kMaxPages + 31) / 32];
+#pragma unroll
+  for (int h = 0; h < (kMaxPages + 31) / 32; ++h)
+    pg[h] = h * 32 + lane < kMaxPages ? slice[1 + h * 32 + lane] : 0;
+  auto page_of = [&](int pi) -> int32_t {  // (pi may differ per lane)
+    int32_t v = 0;
+#pragma unroll
+    for (int h = 0; h < (kMaxPages + 31) / 32; ++h) {
+      const int32_t x = __shfl_sync(kFull, pg[h], pi & 31);
+      if ((pi >> 5) == h) v = x;
+    }
+    return v;
+  };
+  const uint32_t lt = (1u << lane) - 1u;
+  int w = 0;  // entries kept so far (write position <= read position: in place)
+  constexpr int U = kPG / 32;
+  for (int pi = 0; pi * kPG < cnt; ++pi) {
+    const uint4* src = p.pool + ((size_t)(uint32_t)page_of(pi) << 7);
+    uint4 ent[U];
+    Row rows[U];
+    bool valid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      valid[u] = pi * kPG + u * 32 + lane < cnt;
+      ent[u] = valid[u] ? src[u * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) rows[u] = load_row(p.codes_full, KP, (int64_t)ent[u].x);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float e = 0.f;
+#pragma unroll
+      for (int b = 0; b < kMaxK; ++b)
+        if (b < K) e += lut32k[b * m + (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+      const bool keep = valid[u] && e < hiT;
+      const uint32_t km = __ballot_sync(kFull, keep);
+      if (keep) {
+        const int wp = w + __popc(km & lt);
+        // (the page id comes from a shuffle: every lane takes part below)
+        ent[u].y = (uint32_t)wp;
+      }
+      valid[u] = keep;
+      w += __popc(km);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int wp = valid[u] ? (int)ent[u].y : 0;
+      const int32_t pid = page_of(wp >> 7);
+      if (valid[u])
+        p.pool[((size_t)(uint32_t)pid << 7) | (uint32_t)(wp & (kPG - 1))] =
+            make_uint4(ent[u].x, 0u, ent[u].z, ent[u].w);
+    }
+  }
+  if (lane == 0) {
+    slice[0] = w;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), (unsigned long long)cnt);
   }
 }
 
@@ -1614,6 +1673,14 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       ns.refinements = L.refinements;
       ns.insertions = L.insertions;
       ns.thr = L.thr64;
+      if (st.count_mode) {
+        // count mode lists every possible insertion whatever the live
+        // threshold does later: fast < T - Smin with T at the hand-over
+        const double T = he[0];
+        ns.thr = __dadd_ru(__dsub_ru(T, st.smin), fabs(T) * 1e-12);
+        float loT;
+        certified_bounds(T, K, loT, ns.hiT);
+      }
       certified_bounds(ns.thr, F, ns.lo, ns.hi);
       if (st.mt_valid) {  // sigma == 0: the heap maximum's tuple ties at thr exactly
         const Row r = load_fast_row(p.codes_fast, FP, hi[0]);
@@ -1625,7 +1692,6 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       ns.rounds = st.rounds + 1;
       ns.walked = st.walked + walked;
       ns.ntraj = L.ntraj;
-      if (st.count_mode) ns.thr = st.thr;  // (still the valid stale bound: no walks)
       p.qs[q] = ns;
     }
     return;
@@ -1656,7 +1722,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       s[8] = st.pro_cand;
       s[9] = listed;
       s[10] = st.insertions;
-      s[11] = __float_as_int(st.hi);
+      s[11] = p.qs[q].listed_raw;  // count mode: listed before the refine kernel (all rounds)
       s[12] = (p.debug & 4) ? t_work : st.pro_t[0];  // debug bit 2: replay warp-0 timers
       s[13] = (p.debug & 4) ? t_wait : st.pro_t[1];
       s[14] = st.pro_t[2];
@@ -1695,19 +1761,16 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
   const int K = p.K, m = p.m, F = p.F;
   const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
-  const int64_t U = (int64_t)p.Q * p.NR;
-  const bool rmaj = p.range_major != 0;
-  int64_t u0, u1, ustep;
-  if (rmaj) { u0 = blockIdx.x; u1 = U; ustep = gridDim.x; }
-  else { u0 = U * blockIdx.x / gridDim.x; u1 = U * (blockIdx.x + 1) / gridDim.x; ustep = 1; }
+  // units: (count-mode query, range), range-major over the batch's count-mode
+  // queries only, so that a few such queries still spread over every SM
+  const int ncm = p.cm_list[0];
+  const int64_t U = (int64_t)ncm * p.NR;
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);
-  (void)K;
   int cur_q = -1;
-  for (int64_t u = u0; u < u1; u += ustep) {
-    const int q = rmaj ? (int)(u % p.Q) : (int)(u / p.NR);
-    const int r = rmaj ? (int)(u / p.Q) : (int)(u % p.NR);
-    if (!p.qs[q].count_mode) continue;  // (uniform per unit)
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+    const int q = p.cm_list[1 + (int)(u % ncm)];
+    const int r = (int)(u / ncm);
     const int64_t P0 = p.qs[q].P0;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     if (P0 >= r_hi) continue;
@@ -1749,12 +1812,22 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
     double thr = sg ? tr[sg - 1].thr : thr0;
     int64_t next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
     float lo, hi;
-    certified_bounds(thr, F, lo, hi);
+    // integer form of the certified test (fast sums are finite and >= 0, so
+    // float order = bit order): x = bits(f) - bits(lo) is negative iff f < lo,
+    // and 0 <= x < band iff float32 cannot decide (lo <= f < hi)
+    uint32_t lo_b, band_w;
+    auto set_thr = [&]() {
+      certified_bounds(thr, F, lo, hi);
+      lo_b = lo > 0.f ? __float_as_uint(lo) : 0u;  // (NaN / non-positive: nothing is below)
+      band_w = (hi > 0.f ? __float_as_uint(hi) : 0u) - lo_b;
+    };
+    set_thr();
     uint4 a[V];  // the next tile's chunks (register double buffer)
     if (t < w_hi) {
 #pragma unroll
       for (int v = 0; v < V; ++v) a[v] = ldg_stream(codes + t / IPC + lane + v * 32);
     }
+    uint32_t cnt32 = 0;  // fast-path count of this lane (flushed below 2^31)
     for (; t < w_hi; t += TILE) {
       uint4 x[V];
 #pragma unroll
@@ -1768,13 +1841,45 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
         while (sg < nt && tr[sg].pos < t) ++sg;
         thr = sg ? tr[sg - 1].thr : thr0;
         next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
-        certified_bounds(thr, F, lo, hi);
+        set_thr();
       }
       const bool split = next_pos < t + TILE - 1;
       const bool full = t >= start && t + TILE <= w_hi;
+      if (full && !split && !surv) {
+        // fast path: count only.  Pair sums run packed (FADD2), as in the filter.
+        uint32_t c = 0, mn = 0xffffffffu;
+#pragma unroll
+        for (int pr = 0; pr < N / 2; ++pr) {
+          float2 acc[FP];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int idx = 2 * pr + h, v = idx / IPC, j = idx % IPC;
+            const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
+#pragma unroll
+            for (int s2 = 0; s2 < FP; ++s2) {
+              const int byte = j * FP + s2;
+              const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
+              const float val = lds_f32(__byte_perm(wd[byte >> 2], Lp[s2], sel));
+              if (h == 0) acc[s2].x = val; else acc[s2].y = val;
+            }
+          }
+#pragma unroll
+          for (int h = 1; h < FP; h *= 2)
+#pragma unroll
+            for (int s2 = 0; s2 + h < FP; s2 += 2 * h) acc[s2] = __fadd2_rn(acc[s2], acc[s2 + h]);
+          const uint32_t x0 = __float_as_uint(acc[0].x) - lo_b, x1 = __float_as_uint(acc[0].y) - lo_b;
+          c += (x0 >> 31) + (x1 >> 31);
+          mn = min(mn, min(x0, x1));
+        }
+        if (!__any_sync(kFull, mn < band_w)) {
+          cnt32 += c;
+          continue;
+        }
+      }
+      // (rare) edge tiles, a threshold change inside the tile, near-ties, and
+      // every tile when survivor bits are requested: per-item decisions
       const int64_t i0 = t + (int64_t)lane * N;
-      // fast sums of the lane's N items (lane-private gathers, as the filter)
-      float fv[N];
+      unsigned long long bits = 0;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
@@ -1787,37 +1892,18 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
             const uint32_t sel = 0x7604u | ((uint32_t)(byte & 3) << 4);
             f += lds_f32(__byte_perm(wd[byte >> 2], Lp[s2], sel));
           }
-          fv[v * IPC + j] = f;
-        }
-      }
-      unsigned long long bits = 0, band = 0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        bits |= (fv[j] < lo) ? (1ull << j) : 0ull;
-        band |= (fv[j] < hi) ? (1ull << j) : 0ull;
-      }
-      band &= ~bits;  // float32 cannot decide these: float64 below
-      if (!full || split || __any_sync(kFull, band != 0)) {
-        // (rare) edge tiles, a threshold change inside the tile, near-ties
-        bits = 0;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-#pragma unroll
-          for (int j = 0; j < IPC; ++j) {
-            const int64_t i = i0 + v * IPC + j;
-            if (i < start || i >= w_hi) continue;
-            double th = thr;
-            float l2 = lo, h2 = hi;
-            if (split) {
-              const int s3 = seg_of(i);
-              th = s3 ? tr[s3 - 1].thr : thr0;
-              certified_bounds(th, F, l2, h2);
-            }
-            const float f = fv[v * IPC + j];
-            bool ref = f < l2;
-            if (!ref && f < h2) ref = tuple_f64<FP>(chunk_tuple<FP>(x[v], j), lut64f, m, F) < th;
-            if (ref) bits |= 1ull << (v * IPC + j);
+          const int64_t i = i0 + v * IPC + j;
+          if (i < start || i >= w_hi) continue;
+          double th = thr;
+          float l2 = lo, h2 = hi;
+          if (split) {
+            const int s3 = seg_of(i);
+            th = s3 ? tr[s3 - 1].thr : thr0;
+            certified_bounds(th, F, l2, h2);
           }
+          bool ref = f < l2;
+          if (!ref && f < h2) ref = tuple_f64<FP>(chunk_tuple<FP>(x[v], j), lut64f, m, F) < th;
+          if (ref) bits |= 1ull << (v * IPC + j);
         }
       }
       refined += (unsigned long long)__popcll(bits);
@@ -1831,6 +1917,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
         }
       }
     }
+    refined += cnt32;  // (a warp slice holds < 2^31 items)
 #pragma unroll
     for (int o = 16; o; o >>= 1) refined += __shfl_xor_sync(kFull, refined, o);
     if (lane == 0 && refined && p.refinements)
@@ -1883,20 +1970,26 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     if (r > 0 && (e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
     icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ev) cudaEventRecord(ev[2 + 2 * r], s);
+    if (ev) cudaEventRecord(ev[2 + 3 * r], s);
+    if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
+      icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    if (ev) cudaEventRecord(ev[3 + 3 * r], s);
     icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (ev) cudaEventRecord(ev[3 + 2 * r], s);
+    if (ev) cudaEventRecord(ev[4 + 3 * r], s);
   }
   for (int r = p.rounds; ev && r < kMaxRounds; ++r) {  // unused rounds: empty intervals
-    cudaEventRecord(ev[2 + 2 * r], s);
-    cudaEventRecord(ev[3 + 2 * r], s);
+    cudaEventRecord(ev[2 + 3 * r], s);
+    cudaEventRecord(ev[3 + 3 * r], s);
+    cudaEventRecord(ev[4 + 3 * r], s);
   }
   if (FP <= 8 && !p.exact_mode && p.count_used) {  // refinement count of count-mode queries
     icq_count_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  if (ev) cudaEventRecord(ev[2 + 2 * kMaxRounds], s);
+  if (ev) cudaEventRecord(ev[2 + 3 * kMaxRounds], s);
   return cudaSuccess;
 }
 

@@ -40,22 +40,24 @@ struct QState {
                         // trajectory and the count kernel tallies refinements / survivors
   float hiT;            // count mode: certified float32 upper bound of T at P (K terms)
   int32_t ntraj;        // count mode: insertions after P (trajectory entries)
+  double smin;          // count mode: min slow-book sum (rounded down), thr = T - smin
   double thr0;          // count mode: the live threshold at P0
   int64_t P0;           // the prologue end (P moves when a walk hands a query to a new round)
   int64_t walked;       // items walked in order in earlier rounds
+  int64_t listed_raw;   // count mode: entries the filter listed before the refine kernel
   int64_t skipped;      // items the filter did not stream (their slice overflowed:
                         // the replay rescans it from the codes)
 };
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries; the filter indexes by gg >> 7)
-constexpr int kMaxPages = 64;    // pages per slice (more -> the replay rescans the slice)
+constexpr int kMaxPages = 128;   // pages per slice (more -> the replay rescans the slice)
 constexpr int kSliceInts = 4 + kMaxPages;  // count, 3 pad, page ids (16-byte rows)
 constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
 constexpr int64_t kRangeAlign = 32768;
 constexpr int kMaxRounds = 4;  // filter/replay rounds per batch (walks past walk_cap resume)
-constexpr int kProfEvents = 3 + 2 * kMaxRounds;  // + the count kernel  // ranges / padding: whole filter tiles of every warp
+constexpr int kProfEvents = 3 + 3 * kMaxRounds;  // start, prologue, (filter, refine, replay) per round, count
 
 // count mode: the live threshold after an insertion at item pos (items > pos use thr)
 struct TrajEntry {
@@ -83,7 +85,7 @@ struct PipeParams {
   int32_t* pool_top;          // pages handed out
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
   TrajEntry* traj;            // [Q][kMaxTraj] count-mode threshold trajectories
-  unsigned long long* count_acc;  // [Q] count-mode refinements after P
+  int32_t* cm_list;           // [1 + Q] count-mode queries of the batch: count, then query ids
   int64_t pool_pages;
   int64_t n;
   int64_t words;              // survivors bitmap words per query
@@ -103,6 +105,7 @@ struct PipeParams {
   int32_t count_div;          // count mode when the live threshold passes > 1/count_div of the
                               // sampled items (0: never; ICQ_COUNT_MODE=1 forces it)
   int32_t force_count;
+  int64_t count_min;          // ... and would list more than count_min items of the rest
   int32_t count_used;         // count mode possible: launch the count kernel
   int32_t pro_live;           // prologue stop rule counts items under theta (1) or under M (0)
   int32_t sigma_f32;          // numpy promotion of a float32 sigma (see live_thr)
@@ -118,7 +121,8 @@ cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, 
                        int Q, const LutProg* prog_dev, int32_t* err, cudaStream_t s);
 // prologue -> filter -> replay for one batch (icq_pipeline.cu)
 // ev: optional kProfEvents events: before the prologue, after the prologue,
-// then after the filter and the replay of every round
+// after the filter, the refine and the replay kernel of every round, after the
+// count kernel
 cudaError_t launch_pipeline(const PipeParams& p, int FP, int filter_ctas, cudaStream_t s,
                             int* unsupported, cudaEvent_t* ev = nullptr);
 

@@ -33,7 +33,7 @@ STATS_FIELDS = 16
 STATS_NAMES = ("insertions", "replay_candidates", "walked_items", "prologue_end",
                "prologue_cycles", "replay_cycles", "rescanned_slices", "wide_rounds",
                "prologue_f64_scored", "filter_candidates", "prologue_insertions",
-               "filter_hi_f32_bits", "prologue_filter_cycles", "prologue_score_cycles",
+               "refine_inputs", "prologue_filter_cycles", "prologue_score_cycles",
                "prologue_decide_cycles", "filter_skipped_items")
 
 

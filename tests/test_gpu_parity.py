@@ -129,6 +129,10 @@ MODES = {
     # insertions only, refinements / survivors from the count kernel
     "countmode": dict(_F, ICQ_COUNT_MODE="1"),
     "countmode_overflow": dict(_F, ICQ_COUNT_MODE="1", ICQ_POOL_PAGES="2"),
+    # count mode + overflowed slices whose walks hand the query to new rounds
+    # (the later rounds list under T - Smin at the hand-over)
+    "countmode_rounds": dict(_F, ICQ_COUNT_MODE="1", ICQ_POOL_PAGES="2", ICQ_WALK_CAP="1",
+                             ICQ_ROUNDS="4"),
 }
 
 

@@ -95,6 +95,9 @@ def _grown(c, n, seed):
     ("shape_c2", {"ICQ_PRO_LIVE": "1"}),
     ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_RANGE_MAJOR": "1"}),
     ("shape_c4", {"ICQ_COUNT_MODE": "1"}),
+    # count mode with an exhausted pool: overflowed slices, walks, new rounds
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_POOL_PAGES": "8192"}),
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_POOL_PAGES": "4096", "ICQ_WALK_CAP": "65536"}),
 ])
 def test_two_million_vs_oracle(name, knobs, monkeypatch):
     for key, val in knobs.items():
