@@ -454,6 +454,11 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     int64_t pm = h->n / 384;
     if (pm < ((int64_t)1 << 16)) pm = (int64_t)1 << 16;
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
+    // refinement-heavy queries continue in count style (float32 exact
+    // pre-filter, ~1 cycle per item): longer, for a tighter T at the hand-over
+    int64_t pc = h->n / 128;
+    if (pc < p.pro_max) pc = p.pro_max;
+    p.pro_max_cm = p.count_used ? env_i("ICQ_PRO_MAX_CM", pc) : 0;
   }
   {
     // candidate pool: a shared bump allocator of 128-entry pages; when it runs
@@ -464,6 +469,12 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 31;  // <= 32 GiB
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
     p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
+  }
+  {
+    const int64_t mp = env_i("ICQ_MAX_PAGES", kListPages);
+    p.max_pages = (int32_t)(mp < 1 ? 1 : (mp > kListPages ? kListPages : mp));
+    const int64_t mc = env_i("ICQ_MAX_PAGES_CM", kMaxPages);
+    p.max_pages_cm = (int32_t)(mc < 1 ? 1 : (mc > kMaxPages ? kMaxPages : mc));
   }
   const int filter_ctas = (int)env_i("ICQ_FILTER_CTAS", sms);
   // ---- stream-ordered scratch (pool cached across calls) -----------------
@@ -485,7 +496,17 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   const size_t b_sl = al((size_t)Qb * p.NR * kFW * kSliceInts * sizeof(int32_t));
   const size_t b_tr = p.count_used ? al((size_t)Qb * kMaxTraj * sizeof(TrajEntry)) : 0;
   const size_t b_cm = al(sizeof(int32_t) * (1 + (size_t)Qb));
-  const size_t scratch = b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl + b_tr + b_cm;
+  // count-mode lists after the refine kernel, contiguous per query (a query
+  // that does not fit is decided from its slices instead)
+  {
+    int64_t c = (int64_t)Qb << 19;
+    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 28;
+    c = c < lo ? lo : (c > hi_ ? hi_ : c);
+    p.cl_cap = p.count_used ? env_i("ICQ_CL_CAP", c) : 0;
+  }
+  const size_t b_cle = al((size_t)p.cl_cap * sizeof(uint4)), b_clx = al((size_t)p.cl_cap * sizeof(double));
+  const size_t scratch =
+      b_qs + 2 * b_he + b_hi + b_pool + b_top + b_sl + b_tr + b_cm + b_cle + b_clx;
   char* sc = nullptr;
   const bool trace = (p.debug & 32) != 0;  // host-side timing of this call (stderr)
   const auto tr0 = std::chrono::steady_clock::now();
@@ -508,6 +529,10 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.traj = b_tr ? reinterpret_cast<TrajEntry*>(o) : nullptr;
     o += b_tr;
     p.cm_list = reinterpret_cast<int32_t*>(o);
+    o += b_cm;
+    p.cl_ent = reinterpret_cast<uint4*>(o); o += b_cle;
+    p.cl_ex = reinterpret_cast<double*>(o);
+    p.cl_top = reinterpret_cast<unsigned long long*>(p.pool_top + 2);  // (b_top: 256 bytes)
   }
   (void)b_lut;
   icq_status st = ICQ_OK;
@@ -530,6 +555,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
     e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(p.cm_list, 0, sizeof(int32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p.cl_top, 0, sizeof(unsigned long long), s);
     int unsupported = 0;
     cudaEvent_t* ev = nullptr;
     cudaEvent_t evs[kProfEvents];

@@ -107,7 +107,7 @@ __device__ __forceinline__ double tuple_f64(uint2 t, const double* lut64f, int m
 // shared-memory layouts
 // --------------------------------------------------------------------------
 struct ProLayout {
-  uint32_t lut64, lut32, he, hf, hi, cf, ce, cid, ctrl, total;
+  uint32_t lut64, lut32, lut32k, he, hf, hi, cf, ce, cid, ctrl, total;
 };
 __host__ __device__ inline uint32_t al16(uint32_t x) { return (x + 15u) & ~15u; }
 __host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
@@ -115,6 +115,7 @@ __host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
   uint32_t o = 0;
   L.lut64 = o; o = al16(o + (uint32_t)K * m * 8);
   L.lut32 = o; o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 4);
+  L.lut32k = o; o = al16(o + (uint32_t)K * m * 4);
   L.he = o;    o = al16(o + (uint32_t)k * 8);
   L.hf = o;    o = al16(o + (uint32_t)k * 8);
   L.hi = o;    o = al16(o + (uint32_t)k * 4);
@@ -146,7 +147,7 @@ __host__ __device__ inline RepLayout rep_layout(int K, int m, int F, int k) {
   L.wfv = o;   o = al16(o + kWU * 32 * 8);
   L.wfe = o;   o = al16(o + kWU * 32 * 8);
   L.widx = o;  o = al16(o + kWU * 32 * 4);
-  L.meta = o;  o = al16(o + kSG * kSliceInts * 4);
+  L.meta = o;  o = al16(o + kSG * kStageInts * 4);
   L.cum = o;   o = al16(o + (kSG + 1) * 4);
   L.chunks = o; o = al16(o + 512 * 3 * 4);
   L.ring = o;  o = al16(o + kRSlots * kCH * 16);
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   int64_t pro_cand = 0;
   long long tp[3] = {0, 0, 0};
   int64_t nblocks = 0;
-  while (*flag) {
+  while (*flag == 1) {
     const long long ta = clock64();
     ++nblocks;
     const int64_t base = (pos / kProBlock) * kProBlock;
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     //     exact < T.  The first inserting lane ends the window's decided
     //     prefix (the bound moves there); the lanes after it are re-tested
     //     against the new bound.  The heap is the sorted-array WarpHeap.
+    const int64_t ref_before = refinements;
     if (warp == 0) {
       double T = H.top_e();
       double thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
@@ -473,11 +475,21 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
         const int64_t nX = p.pro_live ? (int64_t)(*nL_total) : (int64_t)ncand;
         if (nX * p.pro_div <= nb) more = false;
       }
+      // refinement-heavy (the live threshold itself passes > 1/count_div of
+      // the block and the rest of the database would list > count_min items):
+      // the prologue goes on in count style (phase 2 below)
+      bool heavy = false;
+      if (FP <= 8 && p.pro_max_cm > 0 && !wide && bend < n && bend >= p.pro_min) {
+        const int64_t rb = refinements - ref_before;
+        heavy = p.force_count != 0 ||
+                (p.count_div > 0 && rb * p.count_div > nb &&
+                 (double)rb * (double)(n - bend) > (double)p.count_min * (double)nb);
+      }
       if (lane == 0) {
         *pub_lo = tn.lo; *pub_hi = tn.hi; *pub_thr = tn.thr;
         *pub_hiL = p.pro_live ? hLn : tn.hi;
         *nL_total = 0;
-        *flag = more ? 1 : 0;
+        *flag = heavy ? 2 : (more ? 1 : 0);
       }
     }
     __syncthreads();
@@ -485,6 +497,119 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     tp[0] += tb - ta;
     tp[1] += tc - tb;
     tp[2] += clock64() - tc;
+  }
+
+  // 3'. phase 2 (refinement-heavy queries): blocks in count style.  Only items
+  //     with exact < T can be inserted, so a block is pre-filtered by the
+  //     float32 exact sum of ALL books (certified against hiT, K terms) -- a
+  //     handful of items per block instead of the refined third of it -- and
+  //     warp 0 decides those in order, recording the live threshold after
+  //     every insertion.  Refinements and survivor bits of [P0, n) come from
+  //     the count kernel.  Much cheaper per item than phase 1, so it runs
+  //     longer (pro_max_cm) and hands the filter a tighter T.
+  const bool phase2 = *flag == 2;  // (CTA-uniform: read after the loop's last barrier)
+  int64_t P0 = pos;
+  double thr0_cm = 0.0;
+  int32_t ntraj = 0;
+  __syncthreads();
+  if (phase2) {
+    float* lut32k = reinterpret_cast<float*>(dsm + Ly.lut32k);
+    volatile float* pub_hiT = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 100);
+    for (int i = tid; i < K * m; i += kProThreads) lut32k[i] = __double2float_rn(lut[i]);
+    TrajEntry* traj = p.traj + (size_t)q * kMaxTraj;
+    if (warp == 0) {
+      thr0_cm = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
+      float loT, hT;
+      certified_bounds(H.top_e(), K, loT, hT);
+      if (lane == 0) *pub_hiT = hT;
+    }
+    __syncthreads();
+    while (pos < n && pos < p.pro_max_cm) {
+      ++nblocks;
+      const int64_t base = (pos / kProBlock) * kProBlock;
+      const int64_t bend = min(n, base + kProBlock);
+      const float hT = *pub_hiT;
+      const int64_t i0 = base + (int64_t)tid * 8;
+      Row rows[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rows[j] = load_row(p.codes_full, p.KP, i0 + j);  // (padded rows)
+      uint32_t mask = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float e = 0.f;
+#pragma unroll
+        for (int b = 0; b < kMaxK; ++b)
+          if (b < K) e += lut32k[b * m + (int)((rows[j].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+        const int64_t i = i0 + j;
+        mask |= ((i >= pos) & (i < bend) & (e < hT)) ? (1u << j) : 0u;
+      }
+      const int cnt = __popc(mask);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      int off = incl - cnt, ncand = 0;
+#pragma unroll
+      for (int t = 0; t < kProThreads / 32; ++t) {
+        const int v = wsum[t];
+        off += t < warp ? v : 0;
+        ncand += v;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((mask >> j) & 1u) {
+          cf[off] = fast64(lut, m, F, c.pw, p.fast_books, rows[j]);
+          ce[off] = exact64(lut, m, K, c.pw, rows[j]);
+          cid[off] = (int32_t)(i0 + j);
+          ++off;
+        }
+      }
+      pro_cand += ncand;
+      __syncthreads();
+      if (warp == 0 && ncand > 0) {
+        double T = H.top_e();
+        double thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
+        for (int c0 = 0; c0 < ncand; c0 += 32) {
+          const int ci = c0 + lane;
+          const bool ok = ci < ncand;
+          const double fv = ok ? cf[ci] : 0.0;
+          const double ev = ok ? ce[ci] : 0.0;
+          const int32_t id = ok ? cid[ci] : 0;
+          uint32_t pending = __ballot_sync(kFull, ok);
+          while (pending) {
+            const bool mine = (pending >> lane) & 1u;
+            const bool ins = mine && fv < thr && ev < T;
+            const uint32_t im = __ballot_sync(kFull, ins);
+            if (!im) break;
+            const int first = __ffs(im) - 1;
+            pending &= ~((2u << first) - 1u);
+            const double ne = __shfl_sync(kFull, ev, first);
+            const double nf = __shfl_sync(kFull, fv, first);
+            const int32_t nid = __shfl_sync(kFull, id, first);
+            H.replace_max(ne, nid, nf, lane);
+            T = H.top_e();
+            thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
+            ++insertions;
+            if (lane == 0) {  // items after nid are refined against the new threshold
+              if (ntraj < kMaxTraj) traj[ntraj] = TrajEntry{(int64_t)nid, thr};
+              else atomicOr(p.error, 16);
+            }
+            ++ntraj;
+          }
+        }
+        float loT, hTn;
+        certified_bounds(T, K, loT, hTn);
+        if (lane == 0) *pub_hiT = hTn;
+      }
+      __syncthreads();
+      pos = bend;
+    }
+    if (warp == 0) H.store(lane);
+    __syncthreads();
   }
 
   // 4. hand the state to the filter / replay kernels: the heap sorted
@@ -501,8 +626,8 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   //     cost walks whenever the live threshold rises above theta (in order,
   //     one CTA).  ICQ_LIST_J >= 0 fixes J.
   int listJ = p.list_j;
-  bool count_mode = FP <= 8 && p.force_count != 0 && !wide && pos < n;
-  if (listJ < 0 || p.count_div > 0) {
+  bool count_mode = FP <= 8 && (p.force_count != 0 || phase2) && !wide && (pos < n || phase2);
+  if (!phase2 && (listJ < 0 || p.count_div > 0)) {
     constexpr int kLad = 9;
     const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30};
     float* lad_hi = reinterpret_cast<float*>(cf);        // (cf/ce are free now)
@@ -621,9 +746,9 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       st.count_mode = count_mode ? 1 : 0;
       st.hiT = hiT;
       st.smin = smin_cm;
-      st.ntraj = 0;
-      st.thr0 = live_thr(hf[0], hi[0], p.sigma, k, f32s);
-      st.P0 = pos;
+      st.ntraj = ntraj;
+      st.thr0 = phase2 ? thr0_cm : live_thr(hf[0], hi[0], p.sigma, k, f32s);
+      st.P0 = P0;
       st.ovf_pages = 0;
       st.ovf_pool = 0;
       st.skipped = 0;
@@ -639,6 +764,52 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   }
 }
 
+// Drop, in place and in order, the entries of one slice that cannot be
+// inserted: float32 exact sum e32 >= hiT (exact64 < T implies e32 < hiT).
+// One warp; lut32(b, code) returns the float32 table entry.  Returns the
+// number of entries kept.
+template <typename LutFn>
+__device__ __forceinline__ int refine_slice(uint4* pool, const int32_t* slice, int cnt,
+                                            const uint8_t* codes_full, int KP, int K, float hiT,
+                                            int lane, LutFn lut32) {
+  const uint32_t lt = (1u << lane) - 1u;
+  int w = 0;  // entries kept so far (write position <= read position: in place)
+  constexpr int U = kPG / 32;
+  for (int pi = 0; pi * kPG < cnt; ++pi) {
+    const uint4* src = pool + ((size_t)(uint32_t)slice[1 + pi] << 7);
+    uint4 ent[U];
+    Row rows[U];
+    bool valid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      valid[u] = pi * kPG + u * 32 + lane < cnt;
+      ent[u] = valid[u] ? src[u * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) rows[u] = load_row(codes_full, KP, (int64_t)ent[u].x);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float e = 0.f;
+#pragma unroll
+      for (int b = 0; b < kMaxK; ++b)
+        if (b < K) e += lut32(b, (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu));
+      const bool keep = valid[u] && e < hiT;
+      const uint32_t km = __ballot_sync(kFull, keep);
+      if (keep) ent[u].y = (uint32_t)(w + __popc(km & lt));  // (write position)
+      valid[u] = keep;
+      w += __popc(km);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (valid[u]) {
+        const int wp = (int)ent[u].y;
+        pool[((size_t)(uint32_t)slice[1 + (wp >> 7)] << 7) | (uint32_t)(wp & (kPG - 1))] =
+            make_uint4(ent[u].x, 0u, ent[u].z, ent[u].w);
+      }
+    }
+  }
+  return w;
+}
 // ==========================================================================
 // K3: filter (the streaming hot path)
 // ==========================================================================
@@ -899,7 +1070,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       const int need = (cnt + T + kPG - 1) / kPG - npages;
       int base_pg = 0;
       if (!overflow && need > 0) {
-        if (npages + need > kMaxPages) {
+        // (count-mode slices may list every item: the replay reads them through
+        // the contiguous list, not through the staged page table)
+        if (npages + need > (p.qs[q].count_mode ? p.max_pages_cm : p.max_pages)) {
           overflow = true;
           if (lane == 0) atomicAdd(&p.qs[q].ovf_pages, 1);
         } else {
@@ -981,63 +1154,101 @@ __global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_const
   const int cnt = slice[0];
   if (cnt <= 0) return;  // empty, or overflowed (the replay walks it)
   const float hiT = p.qs[q].hiT;
-  static_assert(kMaxPages <= 128, "page ids of a slice are held by 4 registers per lane");
-  int32_t pg[(kMaxPages + 31) / 32];
-#pragma unroll
-  for (int h = 0; h < (kMaxPages + 31) / 32; ++h)
-    pg[h] = h * 32 + lane < kMaxPages ? slice[1 + h * 32 + lane] : 0;
-  auto page_of = [&](int pi) -> int32_t {  // (pi may differ per lane)
-    int32_t v = 0;
-#pragma unroll
-    for (int h = 0; h < (kMaxPages + 31) / 32; ++h) {
-      const int32_t x = __shfl_sync(kFull, pg[h], pi & 31);
-      if ((pi >> 5) == h) v = x;
-    }
-    return v;
-  };
-  const uint32_t lt = (1u << lane) - 1u;
-  int w = 0;  // entries kept so far (write position <= read position: in place)
-  constexpr int U = kPG / 32;
-  for (int pi = 0; pi * kPG < cnt; ++pi) {
-    const uint4* src = p.pool + ((size_t)(uint32_t)page_of(pi) << 7);
-    uint4 ent[U];
-    Row rows[U];
-    bool valid[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      valid[u] = pi * kPG + u * 32 + lane < cnt;
-      ent[u] = valid[u] ? src[u * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) rows[u] = load_row(p.codes_full, KP, (int64_t)ent[u].x);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      float e = 0.f;
-#pragma unroll
-      for (int b = 0; b < kMaxK; ++b)
-        if (b < K) e += lut32k[b * m + (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
-      const bool keep = valid[u] && e < hiT;
-      const uint32_t km = __ballot_sync(kFull, keep);
-      if (keep) {
-        const int wp = w + __popc(km & lt);
-        // (the page id comes from a shuffle: every lane takes part below)
-        ent[u].y = (uint32_t)wp;
-      }
-      valid[u] = keep;
-      w += __popc(km);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int wp = valid[u] ? (int)ent[u].y : 0;
-      const int32_t pid = page_of(wp >> 7);
-      if (valid[u])
-        p.pool[((size_t)(uint32_t)pid << 7) | (uint32_t)(wp & (kPG - 1))] =
-            make_uint4(ent[u].x, 0u, ent[u].z, ent[u].w);
-    }
-  }
+  const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, K, hiT, lane,
+                             [&](int b, int code) { return lut32k[b * m + code]; });
   if (lane == 0) {
     slice[0] = w;
     atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), (unsigned long long)cnt);
+  }
+}
+
+// K3c: per count-mode query, the offsets of its refined slices in one
+// contiguous list (database order), and the list's place in cl_ent / cl_ex.
+// A query with an overflowed slice, or whose list does not fit the buffer,
+// keeps cl_base = -1: the replay decides it from the slices.
+constexpr int kSliceOff = kSliceInts - 1;  // (the slice row's last int: offset in the list)
+template <int FP>
+__global__ void __launch_bounds__(256) icq_cl_scan_kernel(const __grid_constant__ PipeParams p) {
+  __shared__ int wsum[8];
+  __shared__ int carry_s, bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = blockIdx.x;
+  if (!p.qs[q].count_mode || p.qs[q].done) return;
+  const int NS = p.NR * kFW;
+  int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
+  if (tid == 0) { carry_s = 0; bad_s = 0; }
+  __syncthreads();
+  for (int s0 = 0; s0 < NS; s0 += 256) {
+    const int s = s0 + tid;
+    const int c = s < NS ? qsl[(int64_t)s * kSliceInts] : 0;
+    if (c < 0) bad_s = 1;
+    const int v = c > 0 ? c : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = carry_s + incl - v;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    if (s < NS) qsl[(int64_t)s * kSliceInts + kSliceOff] = off;
+    __syncthreads();
+    if (tid == 255) carry_s = off + v;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const long long total = carry_s;
+    long long base = -1;
+    if (!bad_s) {
+      base = (long long)atomicAdd(p.cl_top, (unsigned long long)total);
+      if (base + total > p.cl_cap) base = -1;
+    }
+    p.qs[q].cl_base = base;
+    p.qs[q].cl_count = total;
+  }
+}
+
+// K3d: gather the refined slices into the query's contiguous list with the
+// float64 exact score of every entry (reference order, exact64) -- the serial
+// replay then streams 24 bytes per entry and reads no code rows.
+template <int FP>
+__global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_constant__ PipeParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  double* lut = reinterpret_cast<double*>(dsm);  // [K][m]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  if (!p.qs[q].count_mode || p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
+  const int64_t r_hi = min(p.n, ((int64_t)r + 1) * p.RS);
+  if (p.qs[q].P >= r_hi) return;
+  const int K = p.K, m = p.m, KP = p.KP;
+  const double* glut = p.lut64 + (size_t)q * K * m;
+  for (int i = tid; i < K * m; i += kFW * 32) lut[i] = glut[i];
+  __syncthreads();
+  const int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+  const int cnt = slice[0];
+  if (cnt <= 0) return;
+  const int64_t dst = p.qs[q].cl_base + slice[kSliceOff];
+  for (int e0 = 0; e0 < cnt; e0 += 64) {
+    uint4 ent[2];
+    Row rows[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = e0 + u * 32 + lane;
+      if (e < cnt) {
+        ent[u] = p.pool[((size_t)(uint32_t)slice[1 + (e >> 7)] << 7) | (uint32_t)(e & (kPG - 1))];
+        rows[u] = load_row(p.codes_full, KP, (int64_t)ent[u].x);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = e0 + u * 32 + lane;
+      if (e < cnt) {
+        p.cl_ent[dst + e] = ent[u];
+        p.cl_ex[dst + e] = exact64(lut, m, K, false, rows[u]);
+      }
+    }
   }
 }
 
@@ -1174,8 +1385,8 @@ __device__ __forceinline__ int replay_window(Live& L, const RCtx& c, int lane,
 // walked the same way (without the early hand-back).
 constexpr int kRW = 4;            // warps per replay CTA
 constexpr int kRP = (kRW - 1) * 32;  // preparing threads
-constexpr int kMaxChunks = 512;   // chunk descriptors per slice group (kSG * kMaxPages * kPG / kCH)
-static_assert(kSG * ((kMaxPages * kPG + kCH - 1) / kCH) <= kMaxChunks,
+constexpr int kMaxChunks = 512;   // chunk descriptors per slice group (kSG * kListPages * kPG / kCH)
+static_assert(kSG * ((kListPages * kPG + kCH - 1) / kCH) <= kMaxChunks,
               "a slice group always fits the chunk descriptors");
 
 template <int FP>
@@ -1428,15 +1639,94 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
     const int NS = p.NR * kFW;  // slices of this query, in database order
     const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
     const int ptid = tid - 32;  // preparing thread index (warps 1..3)
-    for (int g0 = 0; g0 < NS && *sskip < n - 1 && !ctl[16]; g0 += kSG) {
+    // count mode with a contiguous list (K3c/K3d): possible insertions in
+    // database order with their exact scores; warps 1..3 stage chunks, warp 0
+    // decides the entries still under the heap maximum (T never increases)
+    const bool cl = c.count_mode && st.cl_base >= 0;
+    if (cl) {
+      const int64_t total = st.cl_count;
+      const uint4* cle = p.cl_ent + st.cl_base;
+      const double* clx = p.cl_ex + st.cl_base;
+      const int nch = (int)((total + kCH - 1) / kCH);
+      listed += total;
+      auto issue_cl = [&](int ch) {
+        if (ch < nch) {
+          uint4* dst = ring + (ch % kRSlots) * kCH;
+          double* dex = ring_e + (ch % kRSlots) * kCH;
+          const int len = (int)min((int64_t)kCH, total - (int64_t)ch * kCH);
+          for (int i = ptid; i < len; i += kRP) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
+                         "l"(cle + (int64_t)ch * kCH + i)
+                         : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dex + i)),
+                         "l"(clx + (int64_t)ch * kCH + i)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      if (warp > 0) {
+        issue_cl(0);
+        issue_cl(1);
+        issue_cl(2);
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
+      }
+      __syncthreads();
+      for (int ch = 0; ch < nch; ++ch) {
+        if (warp > 0) {
+          issue_cl(ch + 3);
+          asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch + 1 landed
+        } else {
+          const uint4* src = ring + (ch % kRSlots) * kCH;
+          const double* exs = ring_e + (ch % kRSlots) * kCH;
+          const int len = (int)min((int64_t)kCH, total - (int64_t)ch * kCH);
+          for (int w0 = 0; w0 < len; w0 += kWU * 32) {
+            int32_t ids[kWU];
+            uint2 tl[kWU];
+            double exv[kWU];
+            bool valid[kWU];
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < kWU; ++u) {
+              const int e = w0 + u * 32 + lane;
+              const bool ok = e < len;
+              const uint4 ent = ok ? src[e] : make_uint4(0, 0, 0, 0);
+              exv[u] = ok ? exs[e] : 0.0;
+              valid[u] = ok && !(exv[u] >= L.T64);
+              ids[u] = (int32_t)ent.x;
+              tl[u] = make_uint2(0u, 0u);
+              if (valid[u]) {
+                const unsigned long long fb = (unsigned long long)__double_as_longlong(
+                    entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F));
+                tl[u] = make_uint2((uint32_t)fb, (uint32_t)(fb >> 32));
+              }
+              any |= valid[u];
+            }
+            if (!__any_sync(kFull, any)) continue;
+            (void)replay_window<16>(L, c, lane, ids, tl, exv, valid, sid, sidx, sfv, sfe, lutf,
+                                    kInf64, -kInf64);
+          }
+        }
+        __syncthreads();
+      }
+      if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+      if (tid == 0) *sskip = n - 1;
+      __syncthreads();
+    }
+    for (int g0 = 0; !cl && g0 < NS && *sskip < n - 1 && !ctl[16]; g0 += kSG) {
       const int ng = min(kSG, NS - g0);
       {  // group meta (counts + page ids) -> shared memory
-        const int pieces = ng * kSliceInts / 4;
-        const uint4* src = reinterpret_cast<const uint4*>(qsl + (int64_t)g0 * kSliceInts);
-        for (int i = tid; i < pieces; i += kRW * 32)
+        // (the first kStageInts ints of every slice row: count + the page ids
+        // a list-mode slice can hold)
+        constexpr int kPieces = kStageInts / 4;
+        for (int i = tid; i < ng * kPieces; i += kRW * 32) {
+          const int t2 = i / kPieces, w2 = i - t2 * kPieces;
+          const uint4* src =
+              reinterpret_cast<const uint4*>(qsl + (int64_t)(g0 + t2) * kSliceInts) + w2;
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smeta + 4 * i)),
-                       "l"(src + i)
+                       "l"(src)
                        : "memory");
+        }
         asm volatile("cp.async.wait_all;" ::: "memory");
       }
       __syncthreads();
@@ -1446,8 +1736,9 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         int acc = 0, nc = 0, open = -1, dropped = 0;
         for (int t2 = 0; t2 < ng; ++t2) {
           scum[t2] = acc;
-          const int cnt = smeta[t2 * kSliceInts];
-          if (cnt < 0) {
+          const int cnt = smeta[t2 * kStageInts];
+          // (overflowed, or a count-mode slice longer than the staged page table)
+          if (cnt < 0 || cnt > kListPages * kPG) {
             if (nc < kMaxChunks) { chunk[3 * nc] = acc; chunk[3 * nc + 1] = 0; chunk[3 * nc + 2] = t2; ++nc; }
             else dropped = 1;
             open = -1;
@@ -1501,7 +1792,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
                 ++ts;
                 tcnt = scum[ts + 1] - scum[ts];
               }
-              const int32_t* sm = smeta + ts * kSliceInts;
+              const int32_t* sm = smeta + ts * kStageInts;
               const uint4* src = p.pool + (int64_t)sm[1 + e / kPG] * kPG + (e % kPG);
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
                            "l"(src)
@@ -1968,11 +2259,18 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     pr.round = r;
     pr.last_round = r + 1 == p.rounds ? 1 : 0;
     if (r > 0 && (e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
+    if (r > 0 && (e = cudaMemsetAsync(p.cl_top, 0, sizeof(unsigned long long), s)) != cudaSuccess)
+      return e;
     icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2 + 3 * r], s);
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
       icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      // ... made contiguous per query, with float64 exact scores
+      icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      icq_cl_gather_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (ev) cudaEventRecord(ev[3 + 3 * r], s);

@@ -45,14 +45,18 @@ struct QState {
   int64_t P0;           // the prologue end (P moves when a walk hands a query to a new round)
   int64_t walked;       // items walked in order in earlier rounds
   int64_t listed_raw;   // count mode: entries the filter listed before the refine kernel
+  int64_t cl_base;      // count mode: the query's contiguous list [cl_base, cl_base + cl_count)
+  int64_t cl_count;     //   in cl_ent / cl_ex, or cl_base < 0: decide from the slices
   int64_t skipped;      // items the filter did not stream (their slice overflowed:
                         // the replay rescans it from the codes)
 };
 
 constexpr int kFW = 16;          // filter warps per CTA (one slice per warp and range)
 constexpr int kPG = 128;         // candidate pool page (entries; the filter indexes by gg >> 7)
-constexpr int kMaxPages = 128;   // pages per slice (more -> the replay rescans the slice)
-constexpr int kSliceInts = 4 + kMaxPages;  // count, 3 pad, page ids (16-byte rows)
+constexpr int kListPages = 128;  // pages per list-mode slice (more -> the replay walks the slice)
+constexpr int kMaxPages = 512;   // pages per count-mode slice (a 64k-item slice may list every item)
+constexpr int kSliceInts = 4 + kMaxPages;  // slice row: count, page ids, pad / list offset (16-byte rows)
+constexpr int kStageInts = 4 + kListPages;  // the part of a row the replay stages in shared memory
 constexpr int kProThreads = 256;
 constexpr int kProBlock = 2048;  // items per prologue block (8 per thread)
 constexpr int64_t kRangeAlign = 32768;
@@ -86,7 +90,13 @@ struct PipeParams {
   int32_t* slices;            // [Q*NR*kFW][kSliceInts]: count (-1 = overflow), page ids
   TrajEntry* traj;            // [Q][kMaxTraj] count-mode threshold trajectories
   int32_t* cm_list;           // [1 + Q] count-mode queries of the batch: count, then query ids
+  uint4* cl_ent;              // [cl_cap] count-mode lists after the refine kernel, contiguous per
+  double* cl_ex;              //   query in database order, with their float64 exact scores
+  unsigned long long* cl_top; // entries handed out of cl_ent / cl_ex
+  int64_t cl_cap;
   int64_t pool_pages;
+  int32_t max_pages;          // pages per list-mode slice (<= kListPages; tests lower it)
+  int32_t max_pages_cm;       // pages per count-mode slice (<= kMaxPages)
   int64_t n;
   int64_t words;              // survivors bitmap words per query
   int64_t RS;                 // items per range (multiple of kRangeAlign)
@@ -113,6 +123,7 @@ struct PipeParams {
   int32_t round, last_round;  // this launch's round
   int64_t walk_cap;           // an in-order walk longer than this hands the query to the next round
   int64_t pro_min, pro_max;   // prologue length bounds (items)
+  int64_t pro_max_cm;         // refinement-heavy queries: the count-style prologue blocks end here
   uint8_t fast_books[kMaxK];
 };
 

@@ -129,6 +129,14 @@ MODES = {
     # insertions only, refinements / survivors from the count kernel
     "countmode": dict(_F, ICQ_COUNT_MODE="1"),
     "countmode_overflow": dict(_F, ICQ_COUNT_MODE="1", ICQ_POOL_PAGES="2"),
+    # count mode entered in the prologue: count-style blocks (float32 exact
+    # pre-filter, trajectory recorded) up to item 6000 / over the whole database
+    "countmode_phase2": dict(_F, ICQ_COUNT_MODE="1", ICQ_PRO_MAX_CM="6000"),
+    "countmode_phase2_all": dict(_F, ICQ_COUNT_MODE="1", ICQ_PRO_MAX_CM="1073741824"),
+    # count mode with one page per slice: overflowed slices are walked
+    "countmode_pages": dict(_F, ICQ_COUNT_MODE="1", ICQ_MAX_PAGES_CM="1"),
+    # list mode with one page per slice
+    "listpages": dict(_F, ICQ_MAX_PAGES="1", ICQ_LIST_DIV="4"),
     # count mode + overflowed slices whose walks hand the query to new rounds
     # (the later rounds list under T - Smin at the hand-over)
     "countmode_rounds": dict(_F, ICQ_COUNT_MODE="1", ICQ_POOL_PAGES="2", ICQ_WALK_CAP="1",

@@ -98,6 +98,14 @@ def _grown(c, n, seed):
     # count mode with an exhausted pool: overflowed slices, walks, new rounds
     ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_POOL_PAGES": "8192"}),
     ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_POOL_PAGES": "4096", "ICQ_WALK_CAP": "65536"}),
+    # count mode, few pages per slice: overflowed slices, the slice path of the replay
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_MAX_PAGES_CM": "1"}),
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_MAX_PAGES_CM": "2", "ICQ_RANGE_MAJOR": "1"}),
+    # count-style prologue blocks up to 300k items
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_PRO_MAX_CM": "300000"}),
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_PRO_MAX_CM": "300000"}),
+    # count mode, the contiguous list does not fit: decided from the slices
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_CL_CAP": "1000"}),
 ])
 def test_two_million_vs_oracle(name, knobs, monkeypatch):
     for key, val in knobs.items():
