@@ -420,6 +420,11 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
+    // the count kernel sweeps 4 filter ranges at a time when the stream is
+    // larger than L2 (8 MiB of fast codes per range at most)
+    const int64_t mult = env_i("ICQ_COUNT_RANGES", big ? 4 : 1);
+    p.RSC = rs * (mult < 1 ? 1 : mult);
+    p.NRC = (int32_t)((h->n + p.RSC - 1) / p.RSC);
   }
   p.pro_div = (int32_t)env_i("ICQ_PRO_DIV", 512);
   p.debug = (int32_t)env_i("ICQ_DEBUG", 0);  // experiments only; results stay exact
@@ -456,9 +461,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
     // refinement-heavy queries continue in count style (float32 exact
     // pre-filter, ~1 cycle per item): longer, for a tighter T at the hand-over
-    int64_t pc = h->n / 128;
-    if (pc < p.pro_max) pc = p.pro_max;
-    p.pro_max_cm = p.count_used ? env_i("ICQ_PRO_MAX_CM", pc) : 0;
+    // (off by default: the same prefix is listed by a first filter round on
+    // every SM instead, cm_prefix below)
+    p.pro_max_cm = p.count_used ? env_i("ICQ_PRO_MAX_CM", 0) : 0;
+    p.cm_prefix = p.count_used ? env_i("ICQ_CM_PREFIX", h->n / 128) : 0;
+    {
+      const int64_t pe = p.cm_prefix < h->n ? p.cm_prefix : h->n;
+      p.NRD = (p.cm_prefix > 0 && p.rounds >= 2) ? (int32_t)((pe + p.RS - 1) / p.RS) : 0;
+    }
   }
   {
     // candidate pool: a shared bump allocator of 128-entry pages; when it runs
@@ -533,6 +543,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.cl_ent = reinterpret_cast<uint4*>(o); o += b_cle;
     p.cl_ex = reinterpret_cast<double*>(o);
     p.cl_top = reinterpret_cast<unsigned long long*>(p.pool_top + 2);  // (b_top: 256 bytes)
+    p.round_cnt = p.pool_top + 4;
   }
   (void)b_lut;
   icq_status st = ICQ_OK;
@@ -555,7 +566,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     b.stats = stats ? stats + (size_t)q0 * kStats : nullptr;
     e = cudaMemsetAsync(p.pool_top, 0, sizeof(int32_t), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(p.cm_list, 0, sizeof(int32_t), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p.cl_top, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess)  // cl_top and the per-round hand-over counters
+      e = cudaMemsetAsync(p.cl_top, 0, sizeof(unsigned long long) + sizeof(int32_t) * (kMaxRounds + 1), s);
     int unsupported = 0;
     cudaEvent_t* ev = nullptr;
     cudaEvent_t evs[kProfEvents];

@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       // the block and the rest of the database would list > count_min items):
       // the prologue goes on in count style (phase 2 below)
       bool heavy = false;
-      if (FP <= 8 && p.pro_max_cm > 0 && !wide && bend < n && bend >= p.pro_min) {
+      if (FP <= 8 && p.count_used && !wide && bend < n && bend >= p.pro_min) {
         const int64_t rb = refinements - ref_before;
         heavy = p.force_count != 0 ||
                 (p.count_div > 0 && rb * p.count_div > nb &&
@@ -753,6 +753,10 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       st.ovf_pool = 0;
       st.skipped = 0;
       st.listed_raw = 0;
+      // count mode: the first round lists a prefix only; the replay hands the
+      // rest to the next round with the heap (and T) it has by then
+      st.list_end = (count_mode && p.rounds >= 2 && pos < p.cm_prefix) ? min(p.cm_prefix, n) : n;
+      st.dense = st.list_end < n ? 1 : 0;  // (FP <= 8: count mode)
       p.qs[q] = st;
       if (count_mode) p.cm_list[1 + atomicAdd(p.cm_list, 1)] = q;
     }
@@ -848,8 +852,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
 
+  if (p.round > 0 && p.round_cnt[p.round] == 0) return;  // no query was handed to this round
   const int K = p.K, m = p.m, F = p.F;
-  const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
+  const int64_t RS = p.RS, SW = p.RS / kFW;
   const int64_t U = (int64_t)p.Q * p.NR;
   int64_t u0, u1, ustep;
   const bool rmaj = p.range_major != 0 || p.round > 0;
@@ -875,9 +880,13 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
     const uint2 mtup = make_uint2(p.qs[q].mtup[0], p.qs[q].mtup[1]);
     const bool mt_valid = p.qs[q].mt_valid != 0;
     const int wide = p.qs[q].wide;
-    const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
+    // (a count-mode query first lists a prefix [P, list_end) only: its replay
+    // hands the rest to the next round with a much tighter T)
+    const int64_t lend = p.qs[q].list_end;
+    const int64_t r_lo = (int64_t)r * RS, r_hi = min(lend, r_lo + RS);
     int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
-    if (P >= r_hi || p.qs[q].done) {  // decided by the prologue / an earlier round
+    if (P >= r_hi || p.qs[q].done || p.qs[q].dense) {  // decided by the prologue / an earlier
+                                                          // round / later / the dense kernel
       if (lane == 0) slice[0] = 0;
       continue;
     }
@@ -905,7 +914,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
       cur_q = q;
     }
     const int64_t w_lo = r_lo + warp * SW;
-    const int64_t w_hi = min(w_lo + SW, n);
+    const int64_t w_hi = min(w_lo + SW, lend);
     const int64_t start = max(w_lo, P);
     if (start >= w_hi) {
       if (lane == 0) slice[0] = 0;
@@ -1126,6 +1135,97 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
 }
 
 // ==========================================================================
+// K3a: dense prefix (count-mode queries, first round)
+// ==========================================================================
+// A count-mode query leaves the prologue early, with a loose heap: T - Smin
+// would pass nearly every item.  Its first round therefore covers a prefix
+// [P, list_end) only, and lists it here without the fast test: every SM reads
+// the prefix rows (coalesced) and keeps the items whose float32 exact sum is
+// under hiT (the only ones that can be inserted), in order, into the same
+// paged slices the filter fills.  The replay decides them and hands the rest
+// of the database to the next round with a tight T.
+template <int FP>
+__global__ void __launch_bounds__(kFW * 32) icq_dense_kernel(const __grid_constant__ PipeParams p) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  float* lut32k = reinterpret_cast<float*>(dsm);  // [K][m]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  if (!p.qs[q].dense || p.qs[q].done) return;  // (CTA-uniform)
+  const int64_t lend = p.qs[q].list_end, P = p.qs[q].P;
+  const int64_t r_lo = (int64_t)r * p.RS, r_hi = min(lend, r_lo + p.RS);
+  if (P >= r_hi) return;  // (the filter wrote empty slices)
+  const int K = p.K, m = p.m, KP = p.KP, F = p.F;
+  const double* glut = p.lut64 + (size_t)q * K * m;
+  for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
+  __syncthreads();
+  const int64_t SW = p.RS / kFW;
+  const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, lend);
+  const int64_t start = max(w_lo, P);
+  if (start >= w_hi) return;
+  int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+  const float hiT = p.qs[q].hiT;
+  const uint32_t lt = (1u << lane) - 1u;
+  int cnt = 0, npages = 0, pg_last = 0, pg_prev = 0;
+  bool overflow = false;
+  for (int64_t i0 = start; i0 < w_hi && !overflow; i0 += 128) {
+    Row rows[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      rows[u] = load_row(p.codes_full, KP, i < w_hi ? i : start);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      float e = 0.f;
+#pragma unroll
+      for (int b = 0; b < kMaxK; ++b)
+        if (b < K) e += lut32k[b * m + (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+      const bool keep = i < w_hi && e < hiT;
+      const uint32_t km = __ballot_sync(kFull, keep);
+      if (!km || overflow) continue;  // (warp-uniform)
+      const int T = __popc(km);
+      if (cnt + T > npages * kPG) {  // one more page (T <= 32)
+        int pgn = 0;
+        if (npages + 1 > p.max_pages_cm) {
+          overflow = true;
+          if (lane == 0) atomicAdd(&p.qs[q].ovf_pages, 1);
+        } else {
+          if (lane == 0) pgn = atomicAdd(p.pool_top, 1);
+          pgn = __shfl_sync(kFull, pgn, 0);
+          if ((int64_t)pgn + 1 > p.pool_pages) {
+            overflow = true;
+            if (lane == 0) atomicAdd(&p.qs[q].ovf_pool, 1);
+          } else {
+            if (lane == 0) slice[1 + npages] = pgn;
+            pg_prev = pg_last;
+            pg_last = pgn;
+            ++npages;
+          }
+        }
+        if (overflow) continue;
+      }
+      if (keep) {
+        const int pos = cnt + __popc(km & lt);
+        const int pid = (pos >> 7) == npages - 1 ? pg_last : pg_prev;
+        uint32_t tx = 0, ty = 0;  // the fast-code tuple, as the filter stores it
+#pragma unroll
+        for (int s2 = 0; s2 < (FP <= 8 ? FP : 8); ++s2) {
+          if (s2 < F) {
+            const uint32_t c2 = rows[u].byte(p.fast_books[s2]);
+            if (s2 < 4) tx |= c2 << (8 * s2); else ty |= c2 << (8 * (s2 - 4));
+          }
+        }
+        p.pool[((size_t)(uint32_t)pid << 7) | (uint32_t)(pos & (kPG - 1))] =
+            make_uint4((uint32_t)i, 0u, tx, ty);
+      }
+      cnt += T;
+    }
+  }
+  if (lane == 0) slice[0] = overflow ? -1 : cnt;
+}
+
+// ==========================================================================
 // K3b: refine (count-mode queries)
 // ==========================================================================
 // The filter lists, for a count-mode query, every item with
@@ -1142,9 +1242,10 @@ __global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_const
   extern __shared__ __align__(16) uint8_t dsm[];
   float* lut32k = reinterpret_cast<float*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (p.round > 0 && p.round_cnt[p.round] == 0) return;
   const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
   if (!p.qs[q].count_mode || p.qs[q].done) return;  // (CTA-uniform)
-  const int64_t r_hi = min(p.n, ((int64_t)r + 1) * p.RS);
+  const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
   if (p.qs[q].P >= r_hi) return;
   const int K = p.K, m = p.m, KP = p.KP;
   const double* glut = p.lut64 + (size_t)q * K * m;
@@ -1173,6 +1274,7 @@ __global__ void __launch_bounds__(256) icq_cl_scan_kernel(const __grid_constant_
   __shared__ int carry_s, bad_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
+  if (p.round > 0 && p.round_cnt[p.round] == 0) return;
   if (!p.qs[q].count_mode || p.qs[q].done) return;
   const int NS = p.NR * kFW;
   int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
@@ -1219,8 +1321,9 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
   double* lut = reinterpret_cast<double*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  if (p.round > 0 && p.round_cnt[p.round] == 0) return;
   if (!p.qs[q].count_mode || p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
-  const int64_t r_hi = min(p.n, ((int64_t)r + 1) * p.RS);
+  const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
   if (p.qs[q].P >= r_hi) return;
   const int K = p.K, m = p.m, KP = p.KP;
   const double* glut = p.lut64 + (size_t)q * K * m;
@@ -1710,7 +1813,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         __syncthreads();
       }
       if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
-      if (tid == 0) *sskip = n - 1;
+      if (tid == 0) *sskip = st.list_end - 1;
       __syncthreads();
     }
     for (int g0 = 0; !cl && g0 < NS && *sskip < n - 1 && !ctl[16]; g0 += kSG) {
@@ -1908,7 +2011,8 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
           // candidates overflowed this slice's pages: walk its items from the codes
           __syncthreads();
           const int64_t j = g0 + chunk[3 * ch + 2];
-          const int64_t lo = max(max(j * SW, st.P), (int64_t)*sskip + 1), hi_ = min((j + 1) * SW, n);
+          const int64_t lo = max(max(j * SW, st.P), (int64_t)*sskip + 1),
+                        hi_ = min((j + 1) * SW, st.list_end);
           if (lo < hi_) {
             if (tid == 0) ++fallback_slices;
             // (a rescan chunk is never staged: its ring slot (8 KiB of mask
@@ -1947,6 +2051,11 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       __syncthreads();
     }
     if (warp == 0) L.H.store(lane);
+    // the lists covered a prefix only: the rest goes to the next round
+    if (tid == 0 && !ctl[16] && st.list_end < n && !p.last_round) {
+      *sskip = st.list_end - 1;
+      ctl[16] = 1;
+    }
   }
   __syncthreads();
   if (ctl[16]) {
@@ -1981,6 +2090,9 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       ns.ovf_pages = 0;
       ns.ovf_pool = 0;
       ns.rounds = st.rounds + 1;
+      ns.list_end = n;
+      ns.dense = 0;
+      atomicAdd(&p.round_cnt[p.round + 1], 1);
       ns.walked = st.walked + walked;
       ns.ntraj = L.ntraj;
       p.qs[q] = ns;
@@ -2005,7 +2117,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       s[0] = L.insertions;
       s[1] = L.candidates;
       s[2] = st.walked + walked;
-      s[3] = st.P;
+      s[3] = st.P0;  // the prologue end (P moves when a query is handed to a new round)
       s[4] = st.pro_cycles;
       s[5] = clock64() - t0;
       s[6] = fallback_slices | ((int64_t)p.qs[q].ovf_pages << 20) | ((int64_t)p.qs[q].ovf_pool << 40);
@@ -2051,13 +2163,21 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
     Lp[s] = ((uint32_t)(1 + s / G::BPR) << 16) |
             (uint32_t)((s % G::BPR) * 4 * G::R + (lane % G::R) * 4);
   const int K = p.K, m = p.m, F = p.F;
-  const int64_t n = p.n, RS = p.RS, SW = p.RS / kFW;
+  // (ranges of its own, RSC >= RS items: no slices here, and longer units
+  // amortise the per-unit barriers and table staging)
+  const int64_t n = p.n, RS = p.RSC, SW = p.RSC / kFW;
   // units: (count-mode query, range), range-major over the batch's count-mode
   // queries only, so that a few such queries still spread over every SM
   const int ncm = p.cm_list[0];
-  const int64_t U = (int64_t)ncm * p.NR;
+  const int64_t U = (int64_t)ncm * p.NRC;
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);
+  // the trajectory entries of the unit's range, staged per unit (insertions are
+  // sparse after the prologue: a 1M-item range holds a handful)
+  constexpr int kTS = 1024;
+  int64_t* s_pos = reinterpret_cast<int64_t*>(dsm + 16384);  // (lut64f: <= 16 KiB)
+  double* s_thr = reinterpret_cast<double*>(dsm + 16384 + kTS * 8);  // [kTS + 1]: + the threshold before
+  int* s_ctl = reinterpret_cast<int*>(dsm + 16384 + kTS * 16 + 16);
   int cur_q = -1;
   for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     const int q = p.cm_list[1 + (int)(u % ncm)];
@@ -2065,8 +2185,31 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
     const int64_t P0 = p.qs[q].P0;
     const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
     if (P0 >= r_hi) continue;
+    const TrajEntry* tr = p.traj + (size_t)q * kMaxTraj;
+    const int nt = min(p.qs[q].ntraj, kMaxTraj);
+    const double thr0 = p.qs[q].thr0;
+    __syncthreads();  // every warp is done with the previous unit's pages and trajectory
+    if (warp == kFW - 1) {
+      // entries [ta, tb) change the threshold inside (r_start, r_hi): lanes 0/1
+      // search the two ends (number of entries with pos < x)
+      const int64_t x = lane ? r_hi : max(r_lo, P0);
+      int lo2 = 0, hi2 = nt;
+      if (lane < 2)
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (tr[mid].pos < x) lo2 = mid + 1; else hi2 = mid;
+        }
+      const int ta = __shfl_sync(kFull, lo2, 0), tb = __shfl_sync(kFull, lo2, 1);
+      const int c = tb - ta;
+      if (c <= kTS)
+        for (int i = lane; i < c; i += 32) { s_pos[i] = tr[ta + i].pos; s_thr[1 + i] = tr[ta + i].thr; }
+      if (lane == 0) {
+        s_thr[0] = ta ? tr[ta - 1].thr : thr0;
+        s_ctl[0] = ta;
+        s_ctl[1] = c <= kTS ? c : -1;  // (-1: too many, read the global array)
+      }
+    }
     if (q != cur_q) {
-      __syncthreads();
       const double* glut = p.lut64 + (size_t)q * K * m;
       for (int i = tid; i < FP * m; i += kFW * 32) {
         const int s = i / m, j = i - s * m;
@@ -2079,29 +2222,36 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
         const int s = i / m, j = i - s * m;
         lut64f[i] = glut[p.fast_books[s] * m + j];
       }
-      __syncthreads();
       cur_q = q;
     }
-    const TrajEntry* tr = p.traj + (size_t)q * kMaxTraj;
-    const int nt = min(p.qs[q].ntraj, kMaxTraj);
-    const double thr0 = p.qs[q].thr0;
+    __syncthreads();
     uint32_t* surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
     const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, n);
     const int64_t start = max(w_lo, P0);
     unsigned long long refined = 0;
-    // threshold of item i: the last trajectory entry with pos < i (binary search)
+    // local view of the trajectory: entry i of the unit (0 <= i < ne), the
+    // threshold before entry 0 at index -1
+    const int ta = s_ctl[0];
+    const bool glob = s_ctl[1] < 0;
+    const int ne = glob ? nt - ta : s_ctl[1];
+    auto pos_at = [&](int i) -> int64_t { return glob ? tr[ta + i].pos : s_pos[i]; };
+    auto thr_before = [&](int i) -> double {  // threshold of items in (pos[i-1], pos[i]]
+      if (!glob) return s_thr[i];
+      return ta + i ? tr[ta + i - 1].thr : thr0;
+    };
+    // number of the unit's entries with pos < i (items > pos use the entry's threshold)
     auto seg_of = [&](int64_t i) -> int {
-      int lo2 = 0, hi2 = nt;  // number of entries with pos < i
+      int lo2 = 0, hi2 = ne;
       while (lo2 < hi2) {
         const int mid = (lo2 + hi2) >> 1;
-        if (tr[mid].pos < i) lo2 = mid + 1; else hi2 = mid;
+        if (pos_at(mid) < i) lo2 = mid + 1; else hi2 = mid;
       }
       return lo2;
     };
     int64_t t = w_lo + ((start - w_lo) / TILE) * TILE;
     int sg = seg_of(t);  // then advanced monotonically: each change point is crossed once
-    double thr = sg ? tr[sg - 1].thr : thr0;
-    int64_t next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
+    double thr = thr_before(sg);
+    int64_t next_pos = sg < ne ? pos_at(sg) : INT64_MAX;
     float lo, hi;
     // integer form of the certified test (fast sums are finite and >= 0, so
     // float order = bit order): x = bits(f) - bits(lo) is negative iff f < lo,
@@ -2129,9 +2279,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
       }
       // the tile's segment(s): one threshold unless a change point falls inside
       if (next_pos < t) {
-        while (sg < nt && tr[sg].pos < t) ++sg;
-        thr = sg ? tr[sg - 1].thr : thr0;
-        next_pos = sg < nt ? tr[sg].pos : INT64_MAX;
+        while (sg < ne && pos_at(sg) < t) ++sg;
+        thr = thr_before(sg);
+        next_pos = sg < ne ? pos_at(sg) : INT64_MAX;
         set_thr();
       }
       const bool split = next_pos < t + TILE - 1;
@@ -2171,6 +2321,18 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
       // every tile when survivor bits are requested: per-item decisions
       const int64_t i0 = t + (int64_t)lane * N;
       unsigned long long bits = 0;
+      // the lane's own threshold: its N consecutive items are walked in
+      // order, the threshold moves only where a change point is crossed
+      double th = thr;
+      float l2 = lo, h2 = hi;
+      int sgl = sg;
+      int64_t nxt = INT64_MAX;  // items > nxt use the next entry's threshold
+      if (split) {
+        sgl = seg_of(i0);
+        th = thr_before(sgl);
+        certified_bounds(th, F, l2, h2);
+        nxt = sgl < ne ? pos_at(sgl) : INT64_MAX;
+      }
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const uint32_t wd[4] = {x[v].x, x[v].y, x[v].z, x[v].w};
@@ -2184,14 +2346,13 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
             f += lds_f32(__byte_perm(wd[byte >> 2], Lp[s2], sel));
           }
           const int64_t i = i0 + v * IPC + j;
-          if (i < start || i >= w_hi) continue;
-          double th = thr;
-          float l2 = lo, h2 = hi;
-          if (split) {
-            const int s3 = seg_of(i);
-            th = s3 ? tr[s3 - 1].thr : thr0;
+          if (i > nxt) {  // (split tiles only)
+            while (sgl < ne && pos_at(sgl) < i) ++sgl;
+            th = thr_before(sgl);
             certified_bounds(th, F, l2, h2);
+            nxt = sgl < ne ? pos_at(sgl) : INT64_MAX;
           }
+          if (i < start || i >= w_hi) continue;
           bool ref = f < l2;
           if (!ref && f < h2) ref = tuple_f64<FP>(chunk_tuple<FP>(x[v], j), lut64f, m, F) < th;
           if (ref) bits |= 1ull << (v * IPC + j);
@@ -2264,6 +2425,11 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2 + 3 * r], s);
+    if (FP <= 8 && !p.exact_mode && p.count_used && r == 0 && p.NRD > 0) {
+      // count-mode queries: the first round lists a prefix, without the fast test
+      icq_dense_kernel<FP><<<p.Q * p.NRD, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
       icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -45,6 +45,10 @@ struct QState {
   int64_t P0;           // the prologue end (P moves when a walk hands a query to a new round)
   int64_t walked;       // items walked in order in earlier rounds
   int64_t listed_raw;   // count mode: entries the filter listed before the refine kernel
+  int64_t list_end;     // the filter lists items [P, list_end) in this round (count mode: a
+                        // prefix first, then the rest under the tighter T)
+  int32_t dense;        // count mode, first round: the prefix is listed by the dense kernel
+  int32_t pad_;
   int64_t cl_base;      // count mode: the query's contiguous list [cl_base, cl_base + cl_count)
   int64_t cl_count;     //   in cl_ent / cl_ex, or cl_base < 0: decide from the slices
   int64_t skipped;      // items the filter did not stream (their slice overflowed:
@@ -100,6 +104,9 @@ struct PipeParams {
   int64_t n;
   int64_t words;              // survivors bitmap words per query
   int64_t RS;                 // items per range (multiple of kRangeAlign)
+  int64_t RSC;                // items per range of the count kernel (a multiple of RS)
+  int32_t NRC;
+  int32_t NRD;                // ranges the dense prefix kernel covers (count mode, first round)
   double sigma;
   int32_t Q, K, m, KP, F, k;
   int32_t NR;                 // ranges per query
@@ -123,6 +130,8 @@ struct PipeParams {
   int32_t round, last_round;  // this launch's round
   int64_t walk_cap;           // an in-order walk longer than this hands the query to the next round
   int64_t pro_min, pro_max;   // prologue length bounds (items)
+  int64_t cm_prefix;          // count mode: the first round lists items below this position only
+  int32_t* round_cnt;         // [kMaxRounds + 1] queries handed to each round
   int64_t pro_max_cm;         // refinement-heavy queries: the count-style prologue blocks end here
   uint8_t fast_books[kMaxK];
 };

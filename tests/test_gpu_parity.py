@@ -133,6 +133,10 @@ MODES = {
     # pre-filter, trajectory recorded) up to item 6000 / over the whole database
     "countmode_phase2": dict(_F, ICQ_COUNT_MODE="1", ICQ_PRO_MAX_CM="6000"),
     "countmode_phase2_all": dict(_F, ICQ_COUNT_MODE="1", ICQ_PRO_MAX_CM="1073741824"),
+    # count mode in two rounds: the first lists items below 4096 only, its
+    # replay hands the rest to the second round (contiguous lists / slices)
+    "countmode_prefix": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096"),
+    "countmode_prefix_slices": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_CL_CAP="1"),
     # count mode with one page per slice: overflowed slices are walked
     "countmode_pages": dict(_F, ICQ_COUNT_MODE="1", ICQ_MAX_PAGES_CM="1"),
     # list mode with one page per slice

@@ -104,6 +104,10 @@ def _grown(c, n, seed):
     # count-style prologue blocks up to 300k items
     ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_PRO_MAX_CM": "300000"}),
     ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_PRO_MAX_CM": "300000"}),
+    # count mode in two rounds (prefix, then the rest)
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_CM_PREFIX": "300000"}),
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_CM_PREFIX": "500000", "ICQ_CL_CAP": "1000"}),
+    ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_CM_PREFIX": "500000", "ICQ_MAX_PAGES_CM": "2"}),
     # count mode, the contiguous list does not fit: decided from the slices
     ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_CL_CAP": "1000"}),
 ])
