@@ -117,6 +117,31 @@ __device__ __forceinline__ double fast64(const double* lut, int m, int F, bool p
   });
 }
 
+// float32 sum of a code row over a [KP][m] float32 table whose rows b >= K are
+// zero (code rows are zero-padded to KP bytes): the certified pre-test of
+// "exact64 < T" (certified_bounds with K terms; adding the zero rows is exact).
+template <int KPc>
+__device__ __forceinline__ float exact32_row(const float* lut32k, int m, const Row& r) {
+  float e = 0.f;
+#pragma unroll
+  for (int b = 0; b < KPc; ++b) e += lut32k[b * m + (int)((r.w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+  return e;
+}
+__device__ __forceinline__ float exact32_any(const float* lut32k, int m, int KP, const Row& r) {
+  switch (KP) {  // (warp-uniform)
+    case 16: return exact32_row<16>(lut32k, m, r);
+    case 8: return exact32_row<8>(lut32k, m, r);
+    case 4: return exact32_row<4>(lut32k, m, r);
+    case 2: return exact32_row<2>(lut32k, m, r);
+    default: return exact32_row<1>(lut32k, m, r);
+  }
+}
+// stage that table from the float64 LUT of a query (all threads of the CTA)
+__device__ __forceinline__ void stage_lut32k(float* lut32k, const double* glut, int K, int KP, int m,
+                                             int tid, int nthreads) {
+  for (int i = tid; i < KP * m; i += nthreads) lut32k[i] = i < K * m ? __double2float_rn(glut[i]) : 0.f;
+}
+
 // (exact, id) ordering of the reference heap (search.py:140: keys (-exact, -id))
 __device__ __forceinline__ bool key_gt(double e1, int32_t i1, double e2, int32_t i2) {
   // branch-free (no short-circuit): the replay warp's hot compares must not

@@ -115,7 +115,7 @@ __host__ __device__ inline ProLayout pro_layout(int K, int m, int F, int k) {
   uint32_t o = 0;
   L.lut64 = o; o = al16(o + (uint32_t)K * m * 8);
   L.lut32 = o; o = al16(o + (uint32_t)(F > 0 ? F : 1) * m * 4);
-  L.lut32k = o; o = al16(o + (uint32_t)K * m * 4);
+  L.lut32k = o; o = al16(o + (uint32_t)(K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16) * m * 4);
   L.he = o;    o = al16(o + (uint32_t)k * 8);
   L.hf = o;    o = al16(o + (uint32_t)k * 8);
   L.hi = o;    o = al16(o + (uint32_t)k * 4);
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     //     exact < T.  The first inserting lane ends the window's decided
     //     prefix (the bound moves there); the lanes after it are re-tested
     //     against the new bound.  The heap is the sorted-array WarpHeap.
-    const int64_t ref_before = refinements;
+    const int64_t ref_before = refinements, ins_before = insertions;
     if (warp == 0) {
       double T = H.top_e();
       double thr = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
@@ -475,14 +475,19 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
         const int64_t nX = p.pro_live ? (int64_t)(*nL_total) : (int64_t)ncand;
         if (nX * p.pro_div <= nb) more = false;
       }
-      // refinement-heavy (the live threshold itself passes > 1/count_div of
-      // the block and the rest of the database would list > count_min items):
-      // the prologue goes on in count style (phase 2 below)
+      // refinement-heavy: the live threshold itself passes > 1/count_div of
+      // the block, at that rate the rest of the database would list >
+      // count_min items, and the refinements are not just the insertions of
+      // a young heap (those decay as k / position; at small sigma a good part
+      // of the refined items is inserted: > 16 refinements per insertion
+      // means a near-exact heap, hence a tight T).  Such a query leaves the
+      // prologue here, in
+      // count mode (after optional count-style blocks, phase 2 below).
       bool heavy = false;
       if (FP <= 8 && p.count_used && !wide && bend < n && bend >= p.pro_min) {
-        const int64_t rb = refinements - ref_before;
+        const int64_t rb = refinements - ref_before, ib = insertions - ins_before;
         heavy = p.force_count != 0 ||
-                (p.count_div > 0 && rb * p.count_div > nb &&
+                (p.count_div > 0 && rb * p.count_div > nb && rb > 16 * ib &&
                  (double)rb * (double)(n - bend) > (double)p.count_min * (double)nb);
       }
       if (lane == 0) {
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   if (phase2) {
     float* lut32k = reinterpret_cast<float*>(dsm + Ly.lut32k);
     volatile float* pub_hiT = reinterpret_cast<volatile float*>(dsm + Ly.ctrl + 100);
-    for (int i = tid; i < K * m; i += kProThreads) lut32k[i] = __double2float_rn(lut[i]);
+    stage_lut32k(lut32k, lut, K, p.KP, m, tid, kProThreads);
     TrajEntry* traj = p.traj + (size_t)q * kMaxTraj;
     if (warp == 0) {
       thr0_cm = live_thr(H.top_f(), H.top_i(), p.sigma, k, f32s);
@@ -536,10 +541,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       uint32_t mask = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        float e = 0.f;
-#pragma unroll
-        for (int b = 0; b < kMaxK; ++b)
-          if (b < K) e += lut32k[b * m + (int)((rows[j].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+        const float e = exact32_any(lut32k, m, p.KP, rows[j]);
         const int64_t i = i0 + j;
         mask |= ((i >= pos) & (i < bend) & (e < hT)) ? (1u << j) : 0u;
       }
@@ -628,17 +630,25 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
   int listJ = p.list_j;
   bool count_mode = FP <= 8 && (p.force_count != 0 || phase2) && !wide && (pos < n || phase2);
   if (!phase2 && (listJ < 0 || p.count_div > 0)) {
-    constexpr int kLad = 9;
-    const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30};
+    // (rungs 0..8: theta_J; rung 9: T - Smin, what count mode would list)
+    constexpr int kLad = 10;
+    const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30, 0};
     float* lad_hi = reinterpret_cast<float*>(cf);        // (cf/ce are free now)
     int* lad_cnt = reinterpret_cast<int*>(cf + 16);
     if (warp == 0) {
-      for (int r = 0; r < kLad; ++r) {
+      for (int r = 0; r < kLad - 1; ++r) {
         const double A = heap_AJ(hf, k, min(ladder[r], k - 1), lane, nullptr);
         float lo_ = kInf, hi_ = kInf;
         certified_bounds(thr_cover(A, p.sigma, f32s, false), F, lo_, hi_);
         if (lane == 0) { lad_hi[r] = hi_; lad_cnt[r] = 0; }
       }
+      float lo_ = kInf, hi_ = kInf;
+      if (FP <= 8 && p.count_div > 0) {
+        const double sm = smin_rd(lut, K, m, p.fast_books, F, lane);
+        const double T = he[0];
+        certified_bounds(__dadd_ru(__dsub_ru(T, sm), fabs(T) * 1e-12), F, lo_, hi_);
+      }
+      if (lane == 0) { lad_hi[kLad - 1] = hi_; lad_cnt[kLad - 1] = 0; }
     }
     __syncthreads();
     int64_t S = (pos - k) / kProBlock * kProBlock;
@@ -681,14 +691,18 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
     __syncthreads();
     if (p.list_j < 0) {
       listJ = 0;
-      for (int r = 0; r < kLad; ++r)
+      for (int r = 0; r < kLad - 1; ++r)
         if (S > 0 && (int64_t)lad_cnt[r] * p.list_div <= S) listJ = ladder[r];
     }
     listJ = min(listJ, k - 1);
     // refinement-heavy: even the live threshold passes > 1/count_div of the
-    // sample -> the lists would hold the refined items themselves
+    // sample -> the lists would hold the refined items themselves.  Count
+    // mode lists the items under T - Smin instead, which only pays while
+    // that bound is selective (a poor heap -- small sigma, low recall --
+    // leaves T loose: <= 1/8 of the sample, else the query stays in list mode)
     if (FP <= 8 && p.count_div > 0 && S > 0 && (int64_t)lad_cnt[0] * p.count_div > S &&
-        (double)lad_cnt[0] * (double)(n - pos) > (double)p.count_min * (double)S)
+        (double)lad_cnt[0] * (double)(n - pos) > (double)p.count_min * (double)S &&
+        (int64_t)lad_cnt[kLad - 1] * 8 <= S)
       count_mode = true;
     __syncthreads();
   }
@@ -757,6 +771,7 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
       // rest to the next round with the heap (and T) it has by then
       st.list_end = (count_mode && p.rounds >= 2 && pos < p.cm_prefix) ? min(p.cm_prefix, n) : n;
       st.dense = st.list_end < n ? 1 : 0;  // (FP <= 8: count mode)
+      st.cm_end = n;
       p.qs[q] = st;
       if (count_mode) p.cm_list[1 + atomicAdd(p.cm_list, 1)] = q;
     }
@@ -770,12 +785,11 @@ __global__ void __launch_bounds__(kProThreads, 2) icq_prologue_kernel(const __gr
 
 // Drop, in place and in order, the entries of one slice that cannot be
 // inserted: float32 exact sum e32 >= hiT (exact64 < T implies e32 < hiT).
-// One warp; lut32(b, code) returns the float32 table entry.  Returns the
-// number of entries kept.
-template <typename LutFn>
+// One warp; lut32k: the float32 table [KP][m] (zero rows for b >= K).  Returns
+// the number of entries kept.
 __device__ __forceinline__ int refine_slice(uint4* pool, const int32_t* slice, int cnt,
-                                            const uint8_t* codes_full, int KP, int K, float hiT,
-                                            int lane, LutFn lut32) {
+                                            const uint8_t* codes_full, int KP, int m, float hiT,
+                                            int lane, const float* lut32k) {
   const uint32_t lt = (1u << lane) - 1u;
   int w = 0;  // entries kept so far (write position <= read position: in place)
   constexpr int U = kPG / 32;
@@ -793,10 +807,7 @@ __device__ __forceinline__ int refine_slice(uint4* pool, const int32_t* slice, i
     for (int u = 0; u < U; ++u) rows[u] = load_row(codes_full, KP, (int64_t)ent[u].x);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      float e = 0.f;
-#pragma unroll
-      for (int b = 0; b < kMaxK; ++b)
-        if (b < K) e += lut32(b, (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu));
+      const float e = exact32_any(lut32k, m, KP, rows[u]);
       const bool keep = valid[u] && e < hiT;
       const uint32_t km = __ballot_sync(kFull, keep);
       if (keep) ent[u].y = (uint32_t)(w + __popc(km & lt));  // (write position)
@@ -1155,8 +1166,7 @@ __global__ void __launch_bounds__(kFW * 32) icq_dense_kernel(const __grid_consta
   const int64_t r_lo = (int64_t)r * p.RS, r_hi = min(lend, r_lo + p.RS);
   if (P >= r_hi) return;  // (the filter wrote empty slices)
   const int K = p.K, m = p.m, KP = p.KP, F = p.F;
-  const double* glut = p.lut64 + (size_t)q * K * m;
-  for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
+  stage_lut32k(lut32k, p.lut64 + (size_t)q * K * m, K, KP, m, tid, kFW * 32);
   __syncthreads();
   const int64_t SW = p.RS / kFW;
   const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, lend);
@@ -1177,10 +1187,7 @@ __global__ void __launch_bounds__(kFW * 32) icq_dense_kernel(const __grid_consta
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t i = i0 + u * 32 + lane;
-      float e = 0.f;
-#pragma unroll
-      for (int b = 0; b < kMaxK; ++b)
-        if (b < K) e += lut32k[b * m + (int)((rows[u].w[b >> 2] >> ((b & 3) * 8)) & 0xffu)];
+      const float e = exact32_any(lut32k, m, KP, rows[u]);
       const bool keep = i < w_hi && e < hiT;
       const uint32_t km = __ballot_sync(kFull, keep);
       if (!km || overflow) continue;  // (warp-uniform)
@@ -1248,15 +1255,13 @@ __global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_const
   const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
   if (p.qs[q].P >= r_hi) return;
   const int K = p.K, m = p.m, KP = p.KP;
-  const double* glut = p.lut64 + (size_t)q * K * m;
-  for (int i = tid; i < K * m; i += kFW * 32) lut32k[i] = __double2float_rn(glut[i]);
+  stage_lut32k(lut32k, p.lut64 + (size_t)q * K * m, K, KP, m, tid, kFW * 32);
   __syncthreads();
   int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
   const int cnt = slice[0];
   if (cnt <= 0) return;  // empty, or overflowed (the replay walks it)
   const float hiT = p.qs[q].hiT;
-  const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, K, hiT, lane,
-                             [&](int b, int code) { return lut32k[b * m + code]; });
+  const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, m, hiT, lane, lut32k);
   if (lane == 0) {
     slice[0] = w;
     atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), (unsigned long long)cnt);
@@ -2059,9 +2064,73 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
   }
   __syncthreads();
   if (ctl[16]) {
-    // a walk ran past p.walk_cap: hand the query to the next round -- the
-    // heap (sorted descending), the first undecided item and, as the new
-    // list threshold, the live threshold itself (J = 0)
+    // a walk ran past p.walk_cap (or the lists covered a prefix only): hand
+    // the query to the next round -- the heap (sorted descending), the first
+    // undecided item and, as the new list threshold, the live threshold
+    // itself (J = 0)
+    //
+    // Count mode pays only while T - Smin is selective, which takes a
+    // near-exact heap (small sigma / low recall leaves T loose).  With the
+    // heap of the hand-over, sample the last <= 16k decided items: the query
+    // stays in count mode iff the live threshold still passes a long list
+    // AND T - Smin passes <= 1/2; else it goes on in list mode (theta from
+    // the ladder of A_J, as at the prologue end) and the count kernel covers
+    // [P0, cm_end) only.
+    bool to_list = false;
+    double theta_new = 0.0;
+    if (st.count_mode && (!p.force_count || (p.debug & 64))) {  // (debug bit 6: always switch)
+      constexpr int kLad = 10;
+      const int ladder[kLad] = {0, 1, 2, 4, 8, 16, 32, 64, 1 << 30, 0};
+      double* lad_thr = sfv;                            // (the window scratch is free now)
+      int* lad_cnt = reinterpret_cast<int*>(sfe);
+      const int64_t E = (int64_t)*sskip + 1;
+      int64_t S = min((int64_t)16384, E - st.P0);
+      if (warp == 0) {
+        for (int r = 0; r < kLad - 1; ++r) {
+          const double A = heap_AJ(hf, k, min(ladder[r], k - 1), lane, nullptr);
+          if (lane == 0) { lad_thr[r] = thr_cover(A, p.sigma, c.f32, false); lad_cnt[r] = 0; }
+        }
+        if (lane == 0) {
+          const double T = he[0];
+          lad_thr[kLad - 1] = __dadd_ru(__dsub_ru(T, st.smin), fabs(T) * 1e-12);
+          lad_cnt[kLad - 1] = 0;
+        }
+      }
+      __syncthreads();
+      int cnt[kLad];
+#pragma unroll
+      for (int r = 0; r < kLad; ++r) cnt[r] = 0;
+      for (int64_t i = E - S + tid; i < E; i += kRW * 32) {
+        uint2 tup;
+        const double f = fast_at(i, tup);
+#pragma unroll
+        for (int r = 0; r < kLad; ++r) cnt[r] += f < lad_thr[r] ? 1 : 0;
+      }
+#pragma unroll
+      for (int r = 0; r < kLad; ++r) {
+        const int c2 = __reduce_add_sync(kFull, cnt[r]);
+        if (lane == 0 && c2) atomicAdd(&lad_cnt[r], c2);
+      }
+      __syncthreads();
+      // (a query already in count mode stays there more readily than one
+      // enters it: the in-order list replay of a 100M-item database costs more
+      // per listed item than the count pass per streamed item)
+      const bool stay = !(p.debug & 64) && S > 0 && (int64_t)lad_cnt[0] * p.count_div * 4 > S &&
+                        (double)lad_cnt[0] * (double)(n - E) * 4.0 > (double)p.count_min * (double)S &&
+                        (int64_t)lad_cnt[kLad - 1] * 2 <= S;
+      if (!stay) {
+        to_list = true;
+        int J = 0;
+        for (int r = 0; r < kLad - 1; ++r)
+          if (S > 0 && (int64_t)lad_cnt[r] * p.list_div <= S) J = r;
+        if (p.list_j >= 0) {  // (a fixed J: its threshold)
+          J = 0;
+          for (int r = 0; r < kLad - 1; ++r)
+            if (ladder[r] <= p.list_j) J = r;
+        }
+        theta_new = lad_thr[J];
+      }
+    }
     for (int i = tid; i < k; i += kRW * 32) {
       p.heap_e[(size_t)q * k + i] = he[i];
       p.heap_f[(size_t)q * k + i] = hf[i];
@@ -2073,7 +2142,12 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
       ns.refinements = L.refinements;
       ns.insertions = L.insertions;
       ns.thr = L.thr64;
-      if (st.count_mode) {
+      if (st.count_mode && to_list) {
+        ns.count_mode = 0;
+        ns.cm_end = ns.P;  // the count kernel covers [P0, cm_end)
+        ns.thr = theta_new;
+        ns.mt_valid = 0;
+      } else if (st.count_mode) {
         // count mode lists every possible insertion whatever the live
         // threshold does later: fast < T - Smin with T at the hand-over
         const double T = he[0];
@@ -2082,7 +2156,7 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
         certified_bounds(T, K, loT, ns.hiT);
       }
       certified_bounds(ns.thr, F, ns.lo, ns.hi);
-      if (st.mt_valid) {  // sigma == 0: the heap maximum's tuple ties at thr exactly
+      if (ns.mt_valid) {  // sigma == 0: the heap maximum's tuple ties at thr exactly
         const Row r = load_fast_row(p.codes_fast, FP, hi[0]);
         ns.mtup[0] = r.w[0];
         ns.mtup[1] = r.w[1];
@@ -2183,7 +2257,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
     const int q = p.cm_list[1 + (int)(u % ncm)];
     const int r = (int)(u / ncm);
     const int64_t P0 = p.qs[q].P0;
-    const int64_t r_lo = (int64_t)r * RS, r_hi = min(n, r_lo + RS);
+    // (a query that went on in list mode is counted up to cm_end only)
+    const int64_t cend = min(n, p.qs[q].cm_end);
+    const int64_t r_lo = (int64_t)r * RS, r_hi = min(cend, r_lo + RS);
     if (P0 >= r_hi) continue;
     const TrajEntry* tr = p.traj + (size_t)q * kMaxTraj;
     const int nt = min(p.qs[q].ntraj, kMaxTraj);
@@ -2226,7 +2302,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
     }
     __syncthreads();
     uint32_t* surv = p.survivors ? p.survivors + (int64_t)q * p.words : nullptr;
-    const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, n);
+    const int64_t w_lo = r_lo + warp * SW, w_hi = min(w_lo + SW, cend);
     const int64_t start = max(w_lo, P0);
     unsigned long long refined = 0;
     // local view of the trajectory: entry i of the unit (0 <= i < ne), the
@@ -2427,11 +2503,11 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     if (ev) cudaEventRecord(ev[2 + 3 * r], s);
     if (FP <= 8 && !p.exact_mode && p.count_used && r == 0 && p.NRD > 0) {
       // count-mode queries: the first round lists a prefix, without the fast test
-      icq_dense_kernel<FP><<<p.Q * p.NRD, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
+      icq_dense_kernel<FP><<<p.Q * p.NRD, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
-      icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(float), s>>>(pr);
+      icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       // ... made contiguous per query, with float64 exact scores
       icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);

@@ -47,6 +47,8 @@ struct QState {
   int64_t listed_raw;   // count mode: entries the filter listed before the refine kernel
   int64_t list_end;     // the filter lists items [P, list_end) in this round (count mode: a
                         // prefix first, then the rest under the tighter T)
+  int64_t cm_end;       // count mode: the count kernel covers [P0, cm_end) (n unless the query
+                        // went on in list mode at a round hand-over)
   int32_t dense;        // count mode, first round: the prefix is listed by the dense kernel
   int32_t pad_;
   int64_t cl_base;      // count mode: the query's contiguous list [cl_base, cl_base + cl_count)

@@ -137,6 +137,11 @@ MODES = {
     # replay hands the rest to the second round (contiguous lists / slices)
     "countmode_prefix": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096"),
     "countmode_prefix_slices": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_CL_CAP="1"),
+    # count mode for the prefix, then list mode (the hand-over finds T - Smin
+    # unselective; forced here): the count kernel covers [P0, 4096) only
+    "countmode_switch": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_DEBUG="64"),
+    "countmode_switch_j0": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_DEBUG="64",
+                                ICQ_LIST_J="0"),
     # count mode with one page per slice: overflowed slices are walked
     "countmode_pages": dict(_F, ICQ_COUNT_MODE="1", ICQ_MAX_PAGES_CM="1"),
     # list mode with one page per slice
