@@ -295,11 +295,13 @@ def main():
     L = icqb._native.lib()
     L.icq_profile_read(None, None)  # drop anything recorded during warm-up
     L.icq_profile_enable(1)  # CUDA events around each pipeline kernel, launch stream
+    launches0 = int(L.icq_kernel_launches())
     clk.recording = True
     for i in range(args.steps):
         outs.append(step(args.warmup + i, evs[i]))
     clk.sample_now()  # the last steps are still running on the device
     torch.cuda.synchronize()
+    gpu_launches = int(L.icq_kernel_launches()) - launches0  # this library's kernels, timed region
     clk.recording = False
     clk.__exit__(None, None, None)
     L.icq_profile_enable(0)
@@ -338,7 +340,12 @@ def main():
     filter_bytes = (nq * (w.n - p_mean) - skipped) * w.F
     filter_gbs = filter_bytes / t_filter_k / 1e9  # per-GPU filter kernel (this rank)
     hbm_peak, sm_max, peak_kind = _peaks()
-    smem_peak_glps = 148 * 32 * sm_max * 1e6 / 1e9
+    # shared-memory gather peak: conflict-free lane-private LDS.32 measured at
+    # 0.715 warp instructions / clock / SM on this pool's B200s (tools/lds_peak.cu,
+    # profiles/r02_lds_peak.txt); the nominal crossbar rate is 1.0
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    smem_nominal_glps = sms * 32 * sm_max * 1e6 / 1e9
+    smem_peak_glps = 0.715 * smem_nominal_glps
 
     # e2e through the C-ABI host-buffer call (pinned host queries)
     e2e = None
@@ -449,7 +456,13 @@ def main():
                      "algorithmic_bytes_per_launch": filter_bytes / args.steps,
                      "filter_ms_per_launch": t_filter_k / args.steps * 1e3,
                      "filter_share_of_step": t_filter_k / t_total,
-                     "smem_gather_frac": (filter_bytes / t_filter_k / 1e9) / smem_peak_glps},
+                     # the kernel's own bound: F table gathers per streamed item
+                     "gather": {"glookups_per_s": filter_bytes / t_filter_k / 1e9,
+                                "peak_measured": smem_peak_glps, "peak_nominal": smem_nominal_glps,
+                                "frac_of_measured": (filter_bytes / t_filter_k / 1e9) / smem_peak_glps,
+                                "count_kernel_frac_of_measured":
+                                    (None if t_count_k <= 0 else
+                                     (nq * (w.n - p_mean) * w.F / t_count_k / 1e9) / smem_peak_glps)}},
         "kernels_ms_per_step": {"lut": t_lut / args.steps * 1e3,
                                 "prologue": t_pro_k / args.steps * 1e3,
                                 "filter": t_filter_k / args.steps * 1e3,
@@ -458,7 +471,7 @@ def main():
                                 "count": t_count_k / args.steps * 1e3},
         "clocks": clk.summary(),
         "e2e": e2e,
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": gpu_launches,
         "cpu_baseline": cpu,
         "sigma_sweep": sweep,
         "setup_seconds": prep_s,

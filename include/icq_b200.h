@@ -53,6 +53,11 @@ const char* icq_last_error(void);
 /* ABI version (bumped on any signature change). */
 int32_t icq_abi_version(void);
 
+/* Search-path kernels this library launched since it was loaded (LUT build,
+ * prologue, filter / dense / refine / list / replay of every round, count):
+ * bench.py reports the difference over its timed region as gpu_launches. */
+int64_t icq_kernel_launches(void);
+
 /* ---------------------------------------------------------------------------
  * Index: device-resident copy of icq.data.SearchIndex (data.py:193-263).
  *   books : host float32 [K*m*d], row-major (K, m, d)        (data.py:143, :222)

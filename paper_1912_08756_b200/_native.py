@@ -40,6 +40,7 @@ _i64 = C.c_int64
 SIGNATURES = {
     "icq_last_error": (C.c_char_p, []),
     "icq_abi_version": (_i32, []),
+    "icq_kernel_launches": (C.c_int64, []),
     "icq_index_create": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, C.POINTER(_vp)]),
     "icq_index_create_u8": (_i32, [_vp, _i32, _i32, _i32, _vp, _i64, _vp, _i32, C.POINTER(_vp)]),
     "icq_index_create_device": (

@@ -242,7 +242,9 @@ icq_status icq_profile_read(double* ms_out, int32_t* launches) {
   return ICQ_OK;
 }
 
-int32_t icq_abi_version(void) { return 2; }
+int32_t icq_abi_version(void) { return 3; }
+
+int64_t icq_kernel_launches(void) { return (int64_t)icq::kernel_launches(); }
 
 icq_status icq_index_create(const float* books, int32_t K, int32_t m, int32_t d,
                             const uint32_t* codes, int64_t n, const uint32_t* fast, int32_t F,
@@ -320,6 +322,7 @@ icq_status icq_build_lut(icq_index_t h, const double* q, int32_t Q, double* lut,
   CUDA_TRY(cudaMallocAsync((void**)&err, sizeof(int32_t), s));
   cudaError_t e = cudaMemsetAsync(err, 0, sizeof(int32_t), s);
   if (e == cudaSuccess) e = launch_lut(h->books, q, lut, h->K, h->m, h->d, Q, h->prog_dev, err, s);
+  count_kernel_launches(1);
   if (e == cudaSuccess) e = cudaMemcpyAsync(herr, err, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(err, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -551,6 +554,7 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   if (e == cudaSuccess && !lut) {  // K1: the float64 LUTs of every query into the workspace
     double* w = reinterpret_cast<double*>(ws);
     e = launch_lut(h->books, q, w, h->K, h->m, h->d, Q, h->prog_dev, p.error, s);
+    count_kernel_launches(1);
     lut = w;
   }
   if (e != cudaSuccess) st = fail(ICQ_ERR_CUDA, "search setup: %s", cudaGetErrorString(e));

@@ -1,9 +1,15 @@
 // icq_pipeline.cu — dispatch of the prologue -> filter -> replay pipeline over
 // the fast-row width FP (kernels in icq_pipeline.cuh, instantiated in
 // icq_pipe_fp*.cu so the five variants compile in parallel).
+#include <atomic>
+
 #include "icq_common.cuh"
 
 namespace icq {
+
+std::atomic<long long> g_kernel_launches{0};
+void count_kernel_launches(int n) { g_kernel_launches.fetch_add(n, std::memory_order_relaxed); }
+long long kernel_launches() { return g_kernel_launches.load(std::memory_order_relaxed); }
 
 template <int FP>
 cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cudaEvent_t* ev);

@@ -2458,6 +2458,7 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_count_kernel(const __grid_con
 // --------------------------------------------------------------------------
 template <int FP>
 cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cudaEvent_t* ev) {
+  int launched = 0;  // kernels of this batch (icq_kernel_launches)
   using G = FGeo<FP>;
   // kernel attributes once per process (they are per function, not per launch)
   static cudaError_t attr[64];
@@ -2488,6 +2489,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
   if (ev) cudaEventRecord(ev[0], s);
   icq_prologue_kernel<FP><<<p.Q, kProThreads, pl.total, s>>>(p);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
   if (ev) cudaEventRecord(ev[1], s);
   // filter / replay rounds: a query whose walk ran too long resumes in the
   // next round; finished queries cost the later launches nothing
@@ -2500,24 +2502,30 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
       return e;
     icq_filter_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
     if (ev) cudaEventRecord(ev[2 + 3 * r], s);
     if (FP <= 8 && !p.exact_mode && p.count_used && r == 0 && p.NRD > 0) {
       // count-mode queries: the first round lists a prefix, without the fast test
       icq_dense_kernel<FP><<<p.Q * p.NRD, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
     }
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
       icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
       // ... made contiguous per query, with float64 exact scores
       icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
       icq_cl_gather_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
     }
     if (ev) cudaEventRecord(ev[3 + 3 * r], s);
     icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(pr);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
     if (ev) cudaEventRecord(ev[4 + 3 * r], s);
   }
   for (int r = p.rounds; ev && r < kMaxRounds; ++r) {  // unused rounds: empty intervals
@@ -2528,8 +2536,10 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
   if (FP <= 8 && !p.exact_mode && p.count_used) {  // refinement count of count-mode queries
     icq_count_kernel<FP><<<filter_ctas, kFW * 32, G::kSmemEnd - kDynBase, s>>>(p);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++launched;
   }
   if (ev) cudaEventRecord(ev[2 + 3 * kMaxRounds], s);
+  count_kernel_launches(launched);
   return cudaSuccess;
 }
 

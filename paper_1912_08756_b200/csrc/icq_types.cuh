@@ -138,6 +138,9 @@ struct PipeParams {
   uint8_t fast_books[kMaxK];
 };
 
+// kernels launched by this library since it was loaded (icq_kernel_launches)
+void count_kernel_launches(int n);
+long long kernel_launches();
 bool make_lut_prog(int d, LutProg* out);
 cudaError_t launch_lut(const float* books, const double* q, double* lut, int K, int m, int d,
                        int Q, const LutProg* prog_dev, int32_t* err, cudaStream_t s);

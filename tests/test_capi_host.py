@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     for s in _declared_symbols():
         assert hasattr(lib, s), s
         assert s in _native.SIGNATURES, f"{s} declared in the header but not bound"
-    assert lib.icq_abi_version() == 2
+    assert lib.icq_abi_version() == 3
 
 
 def test_null_handle_is_validation_error():
