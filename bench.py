@@ -81,6 +81,7 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         self.recording = False  # rows are kept only while the timed region runs
+        self.periodic = True    # sample from the thread during the timed region
         self._first = threading.Event()
         self._nv = None
         self._h = None
@@ -122,6 +123,13 @@ class ClockSampler:
             if self.recording:
                 self.rows.append((float(sm), float(self._mx), int(rb)))
             self._stop.wait(0.25)
+            # launch-bound steps (a few ms, two dozen launches each): an NVML
+            # query now and then holds a driver lock for 25-110 ms and shows up
+            # as one slow step -- such runs are sampled from the main thread
+            # only (sample_now: before the timed region and while its last
+            # steps still run)
+            while self.recording and not self.periodic and not self._stop.is_set():
+                self._stop.wait(0.05)
 
     def sample_now(self):
         """One sample from the calling thread (short timed regions: taken
@@ -284,9 +292,11 @@ def main():
 
     clk = ClockSampler(local).__enter__()
     clk.wait_started()
+    t_w = time.perf_counter()
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    clk.periodic = (time.perf_counter() - t_w) / max(1, args.warmup) > 0.02
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -297,6 +307,7 @@ def main():
     L.icq_profile_enable(1)  # CUDA events around each pipeline kernel, launch stream
     launches0 = int(L.icq_kernel_launches())
     clk.recording = True
+    clk.sample_now()
     for i in range(args.steps):
         outs.append(step(args.warmup + i, evs[i]))
     clk.sample_now()  # the last steps are still running on the device

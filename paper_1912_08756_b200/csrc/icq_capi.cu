@@ -423,9 +423,9 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
-    // the count kernel sweeps 4 filter ranges at a time when the stream is
-    // larger than L2 (8 MiB of fast codes per range at most)
-    const int64_t mult = env_i("ICQ_COUNT_RANGES", big ? 4 : 1);
+    // the count kernel sweeps 2 filter ranges at a time when the stream is
+    // larger than L2 (measured on c5: 1 -> 22.5, 2 -> 21.5, 4 -> 22.3, 8 -> 24.1 ms)
+    const int64_t mult = env_i("ICQ_COUNT_RANGES", big ? 2 : 1);
     p.RSC = rs * (mult < 1 ? 1 : mult);
     p.NRC = (int32_t)((h->n + p.RSC - 1) / p.RSC);
   }
@@ -515,7 +515,8 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     int64_t c = (int64_t)Qb << 19;
     const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 28;
     c = c < lo ? lo : (c > hi_ ? hi_ : c);
-    p.cl_cap = p.count_used ? env_i("ICQ_CL_CAP", c) : 0;
+    p.cl_cap = env_i("ICQ_CL_CAP", c);
+    p.cl_enable = (int32_t)env_i("ICQ_CL", 1);
   }
   const size_t b_cle = al((size_t)p.cl_cap * sizeof(uint4)), b_clx = al((size_t)p.cl_cap * sizeof(double));
   const size_t scratch =

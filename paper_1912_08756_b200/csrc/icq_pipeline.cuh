@@ -1280,7 +1280,11 @@ __global__ void __launch_bounds__(256) icq_cl_scan_kernel(const __grid_constant_
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
-  if (!p.qs[q].count_mode || p.qs[q].done) return;
+  if (p.qs[q].done) return;
+  if (!p.cl_enable) {  // (ICQ_CL=0: every query is decided from its slices)
+    if (tid == 0) p.qs[q].cl_base = -1;
+    return;
+  }
   const int NS = p.NR * kFW;
   int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
   if (tid == 0) { carry_s = 0; bad_s = 0; }
@@ -1327,7 +1331,7 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
-  if (!p.qs[q].count_mode || p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
+  if (p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
   const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
   if (p.qs[q].P >= r_hi) return;
   const int K = p.K, m = p.m, KP = p.KP;
@@ -1747,79 +1751,124 @@ __global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_co
     const int NS = p.NR * kFW;  // slices of this query, in database order
     const int32_t* qsl = p.slices + (int64_t)q * NS * kSliceInts;
     const int ptid = tid - 32;  // preparing thread index (warps 1..3)
-    // count mode with a contiguous list (K3c/K3d): possible insertions in
-    // database order with their exact scores; warps 1..3 stage chunks, warp 0
-    // decides the entries still under the heap maximum (T never increases)
-    const bool cl = c.count_mode && st.cl_base >= 0;
+    // Contiguous list (K3c/K3d): the query's listed entries in database order
+    // with their float64 exact scores; warps 1..3 stage chunks (cp.async
+    // ring), warp 0 decides.  Count mode: only the entries still under the
+    // heap maximum matter (T never increases) and no walk is ever needed.
+    // List mode: an insertion that lifts the live threshold above theta
+    // starts an in-order walk of the database (all four warps); the list
+    // resumes at the first entry after the last walked item.
+    const bool cl = st.cl_base >= 0;
     if (cl) {
       const int64_t total = st.cl_count;
       const uint4* cle = p.cl_ent + st.cl_base;
       const double* clx = p.cl_ex + st.cl_base;
-      const int nch = (int)((total + kCH - 1) / kCH);
       listed += total;
-      auto issue_cl = [&](int ch) {
-        if (ch < nch) {
-          uint4* dst = ring + (ch % kRSlots) * kCH;
-          double* dex = ring_e + (ch % kRSlots) * kCH;
-          const int len = (int)min((int64_t)kCH, total - (int64_t)ch * kCH);
-          for (int i = ptid; i < len; i += kRP) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
-                         "l"(cle + (int64_t)ch * kCH + i)
-                         : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dex + i)),
-                         "l"(clx + (int64_t)ch * kCH + i)
-                         : "memory");
-          }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      if (warp > 0) {
-        issue_cl(0);
-        issue_cl(1);
-        issue_cl(2);
-        asm volatile("cp.async.wait_group 2;" ::: "memory");
-      }
-      __syncthreads();
-      for (int ch = 0; ch < nch; ++ch) {
-        if (warp > 0) {
-          issue_cl(ch + 3);
-          asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch + 1 landed
-        } else {
-          const uint4* src = ring + (ch % kRSlots) * kCH;
-          const double* exs = ring_e + (ch % kRSlots) * kCH;
-          const int len = (int)min((int64_t)kCH, total - (int64_t)ch * kCH);
-          for (int w0 = 0; w0 < len; w0 += kWU * 32) {
-            int32_t ids[kWU];
-            uint2 tl[kWU];
-            double exv[kWU];
-            bool valid[kWU];
-            bool any = false;
-#pragma unroll
-            for (int u = 0; u < kWU; ++u) {
-              const int e = w0 + u * 32 + lane;
-              const bool ok = e < len;
-              const uint4 ent = ok ? src[e] : make_uint4(0, 0, 0, 0);
-              exv[u] = ok ? exs[e] : 0.0;
-              valid[u] = ok && !(exv[u] >= L.T64);
-              ids[u] = (int32_t)ent.x;
-              tl[u] = make_uint2(0u, 0u);
-              if (valid[u]) {
-                const unsigned long long fb = (unsigned long long)__double_as_longlong(
-                    entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F));
-                tl[u] = make_uint2((uint32_t)fb, (uint32_t)(fb >> 32));
-              }
-              any |= valid[u];
+      int64_t e_base = 0;  // the pipeline (re)starts at this entry
+      for (;;) {
+        const int nch = (int)((total - e_base + kCH - 1) / kCH);
+        auto issue_cl = [&](int ch) {
+          if (ch < nch) {
+            uint4* dst = ring + (ch % kRSlots) * kCH;
+            double* dex = ring_e + (ch % kRSlots) * kCH;
+            const int64_t e0 = e_base + (int64_t)ch * kCH;
+            const int len = (int)min((int64_t)kCH, total - e0);
+            for (int i = ptid; i < len; i += kRP) {
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + i)),
+                           "l"(cle + e0 + i)
+                           : "memory");
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dex + i)),
+                           "l"(clx + e0 + i)
+                           : "memory");
             }
-            if (!__any_sync(kFull, any)) continue;
-            (void)replay_window<16>(L, c, lane, ids, tl, exv, valid, sid, sidx, sfv, sfe, lutf,
-                                    kInf64, -kInf64);
           }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (warp > 0) {
+          issue_cl(0);
+          issue_cl(1);
+          issue_cl(2);
+          asm volatile("cp.async.wait_group 2;" ::: "memory");
         }
         __syncthreads();
+        bool want_walk = false;
+        for (int ch = 0; ch < nch; ++ch) {
+          if (warp > 0) {
+            issue_cl(ch + 3);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");  // chunk ch + 1 landed
+          } else {
+            const uint4* src = ring + (ch % kRSlots) * kCH;
+            const double* exs = ring_e + (ch % kRSlots) * kCH;
+            const int len = (int)min((int64_t)kCH, total - e_base - (int64_t)ch * kCH);
+            for (int w0 = 0; w0 < len; w0 += kWU * 32) {
+              int32_t ids[kWU];
+              uint2 tl[kWU];
+              double exv[kWU];
+              bool valid[kWU];
+              bool any = false;
+#pragma unroll
+              for (int u = 0; u < kWU; ++u) {
+                const int e = w0 + u * 32 + lane;
+                const bool ok = e < len;
+                const uint4 ent = ok ? src[e] : make_uint4(0, 0, 0, 0);
+                exv[u] = ok ? exs[e] : 0.0;
+                // count mode: exact >= T now can never be inserted later
+                valid[u] = ok && !(c.count_mode && exv[u] >= L.T64);
+                ids[u] = (int32_t)ent.x;
+                tl[u] = make_uint2(0u, 0u);
+                if (valid[u]) {
+                  const unsigned long long fb = (unsigned long long)__double_as_longlong(
+                      entry_f64<FP>(make_uint2(ent.z, ent.w), lutf, m, F));
+                  tl[u] = make_uint2((uint32_t)fb, (uint32_t)(fb >> 32));
+                }
+                any |= valid[u];
+              }
+              if (!__any_sync(kFull, any)) continue;
+              const int b2 = replay_window<16>(L, c, lane, ids, tl, exv, valid, sid, sidx, sfv, sfe,
+                                               lutf, c.count_mode ? kInf64 : theta, -kInf64);
+              if (b2 >= 0) {  // the live threshold rose above theta: walk from the next item
+                const int32_t y = __shfl_sync(kFull, ids[b2 >> 5], b2 & 31);
+                if (lane == 0) { *walk_from = (long long)y + 1; ctl[3] = 1; }
+                break;
+              }
+            }
+            if (lane == 0) *pub_thr = L.thr64;
+          }
+          __syncthreads();
+          if (ctl[3]) { want_walk = true; break; }  // (CTA-uniform)
+        }
+        if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (!want_walk) {
+          if (tid == 0) *sskip = st.list_end - 1;
+          __syncthreads();
+          break;
+        }
+        const int64_t from = (int64_t)*walk_from;
+        __syncthreads();
+        if (tid == 0) ctl[3] = 0;
+        // scratch: two exact-score slots of the (drained) ring
+        walk(from, st.list_end, true, reinterpret_cast<uint32_t*>(ring_e),
+             reinterpret_cast<int32_t*>(ring_e + kCH), kCH * 8 * 8);
+        if (*sskip >= st.list_end - 1 || ctl[16]) break;  // walked to the end / handed over
+        if (tid == 0) {  // resume at the first entry after the last walked item
+          const int64_t skp = (int64_t)*sskip;
+          int64_t lo2 = e_base, hi2 = total;
+          while (lo2 < hi2) {
+            const int64_t mid = (lo2 + hi2) >> 1;
+            if ((int64_t)cle[mid].x <= skp) lo2 = mid + 1; else hi2 = mid;
+          }
+          *snext = (long long)lo2;
+        }
+        __syncthreads();
+        e_base = (int64_t)*snext;
+        __syncthreads();
+        if (e_base >= total) {
+          if (tid == 0) *sskip = st.list_end - 1;
+          __syncthreads();
+          break;
+        }
       }
-      if (warp > 0) asm volatile("cp.async.wait_all;" ::: "memory");
-      if (tid == 0) *sskip = st.list_end - 1;
-      __syncthreads();
     }
     for (int g0 = 0; !cl && g0 < NS && *sskip < n - 1 && !ctl[16]; g0 += kSG) {
       const int ng = min(kSG, NS - g0);
@@ -2514,13 +2563,14 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
       icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++launched;
-      // ... made contiguous per query, with float64 exact scores
+    }
+    {  // the lists made contiguous per query, with float64 exact scores
       icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++launched;
+      ++launched;
       icq_cl_gather_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++launched;
+      ++launched;
     }
     if (ev) cudaEventRecord(ev[3 + 3 * r], s);
     icq_replay_kernel<FP><<<p.Q, kRW * 32, rl.total, s>>>(pr);

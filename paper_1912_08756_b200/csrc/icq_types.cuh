@@ -100,6 +100,7 @@ struct PipeParams {
   double* cl_ex;              //   query in database order, with their float64 exact scores
   unsigned long long* cl_top; // entries handed out of cl_ent / cl_ex
   int64_t cl_cap;
+  int32_t cl_enable;          // 0: no contiguous lists (ICQ_CL=0, tests of the slice path)
   int64_t pool_pages;
   int32_t max_pages;          // pages per list-mode slice (<= kListPages; tests lower it)
   int32_t max_pages_cm;       // pages per count-mode slice (<= kMaxPages)

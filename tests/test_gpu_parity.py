@@ -142,6 +142,14 @@ MODES = {
     "countmode_switch": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_DEBUG="64"),
     "countmode_switch_j0": dict(_F, ICQ_COUNT_MODE="1", ICQ_CM_PREFIX="4096", ICQ_DEBUG="64",
                                 ICQ_LIST_J="0"),
+    # the slice path of the replay (no contiguous lists): list threshold
+    # variants, the preparing warps' debug modes, rounds, count mode
+    "slices_filter": dict(_F, ICQ_CL="0"),
+    "slices_listj0": dict(_F, ICQ_LIST_J="0", ICQ_CL="0"),
+    "slices_noprep": dict(_F, ICQ_DEBUG="2", ICQ_CL="0"),
+    "slices_allexact": dict(_F, ICQ_DEBUG="8", ICQ_CL="0"),
+    "slices_rounds": dict(_F, ICQ_WALK_CAP="1", ICQ_ROUNDS="4", ICQ_CL="0"),
+    "slices_countmode": dict(_F, ICQ_COUNT_MODE="1", ICQ_CL="0"),
     # count mode with one page per slice: overflowed slices are walked
     "countmode_pages": dict(_F, ICQ_COUNT_MODE="1", ICQ_MAX_PAGES_CM="1"),
     # list mode with one page per slice
