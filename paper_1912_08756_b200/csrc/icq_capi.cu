@@ -425,6 +425,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     p.NR = (int32_t)((h->n + rs - 1) / rs);
     // the count kernel sweeps 2 filter ranges at a time when the stream is
     // larger than L2 (measured on c5: 1 -> 22.5, 2 -> 21.5, 4 -> 22.3, 8 -> 24.1 ms)
+    // refine / gather CTAs (one warp per slice of a range) can take a group of
+    // ranges each, staging their tables once per CTA; measured no gain on c4
+    // and a loss on c5 (fewer warps with row reads in flight): one range each
+    {
+      p.RG = (int32_t)env_i("ICQ_RANGE_GROUP", 1);
+      if (p.RG < 1) p.RG = 1;
+      p.NRG = (p.NR + p.RG - 1) / p.RG;
+    }
     const int64_t mult = env_i("ICQ_COUNT_RANGES", big ? 2 : 1);
     p.RSC = rs * (mult < 1 ? 1 : mult);
     p.NRC = (int32_t)((h->n + p.RSC - 1) / p.RSC);

@@ -1250,22 +1250,26 @@ __global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_const
   float* lut32k = reinterpret_cast<float*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
-  const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  // one CTA per (query, group of RG ranges): the table is staged once per CTA
+  const int q = (int)(blockIdx.x % (unsigned)p.Q), rg = (int)(blockIdx.x / (unsigned)p.Q);
   if (!p.qs[q].count_mode || p.qs[q].done) return;  // (CTA-uniform)
-  const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
-  if (p.qs[q].P >= r_hi) return;
+  const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
+  if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) return;
   const int K = p.K, m = p.m, KP = p.KP;
   stage_lut32k(lut32k, p.lut64 + (size_t)q * K * m, K, KP, m, tid, kFW * 32);
   __syncthreads();
-  int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
-  const int cnt = slice[0];
-  if (cnt <= 0) return;  // empty, or overflowed (the replay walks it)
   const float hiT = p.qs[q].hiT;
-  const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, m, hiT, lane, lut32k);
-  if (lane == 0) {
-    slice[0] = w;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), (unsigned long long)cnt);
+  unsigned long long raw = 0;
+  for (int r = r0; r < r1; ++r) {
+    int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+    const int cnt = slice[0];
+    if (cnt <= 0) continue;  // empty, or overflowed (the replay walks it)
+    const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, m, hiT, lane, lut32k);
+    if (lane == 0) slice[0] = w;
+    raw += (unsigned long long)cnt;
   }
+  if (lane == 0 && raw)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), raw);
 }
 
 // K3c: per count-mode query, the offsets of its refined slices in one
@@ -1329,18 +1333,19 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
   extern __shared__ __align__(16) uint8_t dsm[];
   double* lut = reinterpret_cast<double*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = (int)(blockIdx.x % (unsigned)p.Q), r = (int)(blockIdx.x / (unsigned)p.Q);
+  const int q = (int)(blockIdx.x % (unsigned)p.Q), rg = (int)(blockIdx.x / (unsigned)p.Q);
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
   if (p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
-  const int64_t r_hi = min(p.qs[q].list_end, ((int64_t)r + 1) * p.RS);
-  if (p.qs[q].P >= r_hi) return;
+  const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
+  if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) return;
   const int K = p.K, m = p.m, KP = p.KP;
   const double* glut = p.lut64 + (size_t)q * K * m;
   for (int i = tid; i < K * m; i += kFW * 32) lut[i] = glut[i];
   __syncthreads();
+  for (int r = r0; r < r1; ++r) {
   const int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
   const int cnt = slice[0];
-  if (cnt <= 0) return;
+  if (cnt <= 0) continue;
   const int64_t dst = p.qs[q].cl_base + slice[kSliceOff];
   for (int e0 = 0; e0 < cnt; e0 += 64) {
     uint4 ent[2];
@@ -1361,6 +1366,7 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
         p.cl_ex[dst + e] = exact64(lut, m, K, false, rows[u]);
       }
     }
+  }
   }
 }
 
@@ -2560,7 +2566,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     ++launched;
     }
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
-      icq_refine_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
+      icq_refine_kernel<FP><<<p.Q * p.NRG, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++launched;
     }
@@ -2568,7 +2574,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
       icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++launched;
-      icq_cl_gather_kernel<FP><<<p.Q * p.NR, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
+      icq_cl_gather_kernel<FP><<<p.Q * p.NRG, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++launched;
     }

@@ -109,6 +109,7 @@ struct PipeParams {
   int64_t RS;                 // items per range (multiple of kRangeAlign)
   int64_t RSC;                // items per range of the count kernel (a multiple of RS)
   int32_t NRC;
+  int32_t RG, NRG;            // ranges per refine / gather CTA, and the number of such groups
   int32_t NRD;                // ranges the dense prefix kernel covers (count mode, first round)
   double sigma;
   int32_t Q, K, m, KP, F, k;

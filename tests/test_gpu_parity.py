@@ -150,6 +150,9 @@ MODES = {
     "slices_allexact": dict(_F, ICQ_DEBUG="8", ICQ_CL="0"),
     "slices_rounds": dict(_F, ICQ_WALK_CAP="1", ICQ_ROUNDS="4", ICQ_CL="0"),
     "slices_countmode": dict(_F, ICQ_COUNT_MODE="1", ICQ_CL="0"),
+    # refine / gather CTAs over groups of 3 ranges
+    "rangegroup": dict(_F, ICQ_RANGE_ITEMS="32768", ICQ_RANGE_GROUP="3"),
+    "countmode_rangegroup": dict(_F, ICQ_COUNT_MODE="1", ICQ_RANGE_ITEMS="32768", ICQ_RANGE_GROUP="3"),
     # count mode with one page per slice: overflowed slices are walked
     "countmode_pages": dict(_F, ICQ_COUNT_MODE="1", ICQ_MAX_PAGES_CM="1"),
     # list mode with one page per slice

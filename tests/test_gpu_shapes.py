@@ -111,6 +111,9 @@ def _grown(c, n, seed):
     # count mode for a prefix, list mode for the rest (forced switch at the hand-over)
     ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_CM_PREFIX": "300000", "ICQ_DEBUG": "64"}),
     ("shape_c4", {"ICQ_COUNT_MODE": "1", "ICQ_CM_PREFIX": "500000", "ICQ_DEBUG": "64"}),
+    # refine / gather CTAs over groups of 7 ranges
+    ("shape_c4", {"ICQ_RANGE_GROUP": "7"}),
+    ("shape_c5", {"ICQ_COUNT_MODE": "1", "ICQ_RANGE_GROUP": "7"}),
     # the slice path of the replay
     ("shape_c4", {"ICQ_CL": "0"}),
     ("shape_c5", {"ICQ_CL": "0", "ICQ_RANGE_MAJOR": "1"}),
