@@ -39,6 +39,11 @@
 #ifndef ICQ_PREFETCH_TILES
 #define ICQ_PREFETCH_TILES 0
 #endif
+// candidate mask of the filter: 1 = one funnel shift per item (ALU pipe),
+// 0 = Horner multiply-adds (two FMA-pipe instructions per item)
+#ifndef ICQ_MASK_SHF
+#define ICQ_MASK_SHF 1
+#endif
 
 #include "icq_common.cuh"
 
@@ -878,7 +883,9 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
   }
   const uint4* codes = reinterpret_cast<const uint4*>(p.codes_fast);
   double* lut64f = reinterpret_cast<double*>(dsm);  // [F][m] below the first page
+#if !ICQ_MASK_SHF
   const uint32_t two = 2u + (uint32_t)(p.n < 0);    // 2, opaque to the compiler (keeps IMADs)
+#endif
   const uint32_t lt_mask = (1u << lane) - 1u;
   int cur_q = -1;
   for (int64_t u = u0; u < u1; u += ustep) {
@@ -1026,7 +1033,11 @@ __global__ void __launch_bounds__(kFW * 32, 1) icq_filter_kernel(const __grid_co
           for (int i = L - 1; i >= 0; --i) {
             const int idx = c * L + i;
             const float dd = (idx & 1) ? d2[idx >> 1].y : d2[idx >> 1].x;
+#if ICQ_MASK_SHF
+            acc[c] = __funnelshift_l(__float_as_uint(dd), acc[c], 1);  // (acc << 1) | sign(d)
+#else
             acc[c] = acc[c] * two + __umulhi(__float_as_uint(dd), two);
+#endif
           }
         }
         uint32_t mk = acc[0];
