@@ -17,7 +17,8 @@ for K in $KERNELS; do
   SKIP=3
   # second batch, second round: count-mode queries list the bulk of the
   # database in round 1 (round 0 is the dense prefix)
-  case $K in icq_filter|icq_refine|icq_replay|icq_cl_gather|icq_cl_scan) SKIP=5;; esac
+  # (ROUND_SKIP=4 for a config whose queries stay in list mode: round 0 is their filter)
+  case $K in icq_filter|icq_refine|icq_replay|icq_cl_gather|icq_cl_scan) SKIP=${ROUND_SKIP:-5};; esac
   ncu --set full --clock-control none --import-source on -k regex:$K -s $SKIP -c 1 \
       -o gpurun_out/full_${CFG}_${TAG}_${K} $CMD > gpurun_out/ncu_full_${CFG}_${K}.log 2>&1
 done
