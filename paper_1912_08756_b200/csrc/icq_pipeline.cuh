@@ -1261,26 +1261,31 @@ __global__ void __launch_bounds__(kFW * 32) icq_refine_kernel(const __grid_const
   float* lut32k = reinterpret_cast<float*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
-  // one CTA per (query, group of RG ranges): the table is staged once per CTA
-  const int q = (int)(blockIdx.x % (unsigned)p.Q), rg = (int)(blockIdx.x / (unsigned)p.Q);
-  if (!p.qs[q].count_mode || p.qs[q].done) return;  // (CTA-uniform)
-  const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
-  if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) return;
+  // units (query, group of RG ranges), query fastest; the table is staged once per unit
   const int K = p.K, m = p.m, KP = p.KP;
-  stage_lut32k(lut32k, p.lut64 + (size_t)q * K * m, K, KP, m, tid, kFW * 32);
-  __syncthreads();
-  const float hiT = p.qs[q].hiT;
-  unsigned long long raw = 0;
-  for (int r = r0; r < r1; ++r) {
-    int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
-    const int cnt = slice[0];
-    if (cnt <= 0) continue;  // empty, or overflowed (the replay walks it)
-    const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, m, hiT, lane, lut32k);
-    if (lane == 0) slice[0] = w;
-    raw += (unsigned long long)cnt;
+  const int64_t U = (int64_t)p.Q * p.NRG;
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+    const int q = (int)(u % p.Q), rg = (int)(u / p.Q);
+    // (the dense prefix kernel already applied this test to what it listed)
+    if (!p.qs[q].count_mode || p.qs[q].done || p.qs[q].dense) continue;  // (CTA-uniform)
+    const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
+    if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) continue;
+    __syncthreads();  // every warp is done with the previous unit's table
+    stage_lut32k(lut32k, p.lut64 + (size_t)q * K * m, K, KP, m, tid, kFW * 32);
+    __syncthreads();
+    const float hiT = p.qs[q].hiT;
+    unsigned long long raw = 0;
+    for (int r = r0; r < r1; ++r) {
+      int32_t* slice = p.slices + ((int64_t)(q * p.NR + r) * kFW + warp) * kSliceInts;
+      const int cnt = slice[0];
+      if (cnt <= 0) continue;  // empty, or overflowed (the replay walks it)
+      const int w = refine_slice(p.pool, slice, cnt, p.codes_full, KP, m, hiT, lane, lut32k);
+      if (lane == 0) slice[0] = w;
+      raw += (unsigned long long)cnt;
+    }
+    if (lane == 0 && raw)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), raw);
   }
-  if (lane == 0 && raw)
-    atomicAdd(reinterpret_cast<unsigned long long*>(&p.qs[q].listed_raw), raw);
 }
 
 // K3c: per count-mode query, the offsets of its refined slices in one
@@ -1344,12 +1349,15 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
   extern __shared__ __align__(16) uint8_t dsm[];
   double* lut = reinterpret_cast<double*>(dsm);  // [K][m]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = (int)(blockIdx.x % (unsigned)p.Q), rg = (int)(blockIdx.x / (unsigned)p.Q);
   if (p.round > 0 && p.round_cnt[p.round] == 0) return;
-  if (p.qs[q].done || p.qs[q].cl_base < 0) return;  // (CTA-uniform)
-  const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
-  if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) return;
   const int K = p.K, m = p.m, KP = p.KP;
+  const int64_t U = (int64_t)p.Q * p.NRG;
+  for (int64_t un = blockIdx.x; un < U; un += gridDim.x) {
+  const int q = (int)(un % p.Q), rg = (int)(un / p.Q);
+  if (p.qs[q].done || p.qs[q].cl_base < 0) continue;  // (CTA-uniform)
+  const int r0 = rg * p.RG, r1 = min(p.NR, r0 + p.RG);
+  if (p.qs[q].P >= min(p.qs[q].list_end, (int64_t)r1 * p.RS)) continue;
+  __syncthreads();  // every warp is done with the previous unit's table
   const double* glut = p.lut64 + (size_t)q * K * m;
   for (int i = tid; i < K * m; i += kFW * 32) lut[i] = glut[i];
   __syncthreads();
@@ -1377,6 +1385,7 @@ __global__ void __launch_bounds__(kFW * 32) icq_cl_gather_kernel(const __grid_co
         p.cl_ex[dst + e] = exact64(lut, m, K, false, rows[u]);
       }
     }
+  }
   }
   }
 }
@@ -2559,6 +2568,10 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
   if (ev) cudaEventRecord(ev[1], s);
   // filter / replay rounds: a query whose walk ran too long resumes in the
   // next round; finished queries cost the later launches nothing
+  // refine / gather: units (query, range group) over a bounded grid (rounds
+  // nobody was handed to cost a few thousand CTA exits, not Q x NR)
+  const int64_t units = (int64_t)p.Q * p.NRG;
+  const unsigned unit_grid = (unsigned)(units < 8192 ? (units < 1 ? 1 : units) : 8192);
   for (int r = 0; r < p.rounds; ++r) {
     PipeParams pr = p;
     pr.round = r;
@@ -2577,7 +2590,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
     ++launched;
     }
     if (FP <= 8 && !p.exact_mode && p.count_used) {  // count-mode lists: possible insertions only
-      icq_refine_kernel<FP><<<p.Q * p.NRG, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
+      icq_refine_kernel<FP><<<unit_grid, kFW * 32, (size_t)p.KP * p.m * sizeof(float), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++launched;
     }
@@ -2585,7 +2598,7 @@ cudaError_t launch_fp(const PipeParams& p, int filter_ctas, cudaStream_t s, cuda
       icq_cl_scan_kernel<FP><<<p.Q, 256, 0, s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++launched;
-      icq_cl_gather_kernel<FP><<<p.Q * p.NRG, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
+      icq_cl_gather_kernel<FP><<<unit_grid, kFW * 32, (size_t)p.K * p.m * sizeof(double), s>>>(pr);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++launched;
     }
