@@ -273,8 +273,10 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
+    from paper_1912_08756_b200.replicas import aggregate, rank_batch
+
     def batch(i):
-        b = (rank + i * world) % nbatches
+        b = rank_batch(rank, world, i, nbatches)
         return Qall[b * B:(b + 1) * B]
 
     def step(i, ev=None):
@@ -334,15 +336,7 @@ def main():
     nq = sum(o[0] for o in outs)
     refine = torch.cat([o[1]["refinements"] for o in outs]).double()
     stats = torch.cat([o[1]["stats"] for o in outs]).double()
-    if dist:
-        tt = torch.tensor([t_total, t_scan, t_lut], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_total, t_scan, t_lut = tt.tolist()
-        nqt = torch.tensor([nq], dtype=torch.float64, device="cuda")
-        dist.all_reduce(nqt)
-        nq_all = int(nqt.item())
-    else:
-        nq_all = nq
+    nq_all, (t_total, t_scan, t_lut) = aggregate(dist, "cuda", nq, [t_total, t_scan, t_lut])
     qps = nq_all / t_total
     lookups = nq * w.n * w.F
     # the filter kernel streams the fast codes of items [P, n) of every query
@@ -377,11 +371,8 @@ def main():
             if i >= args.warmup:
                 e2e_t += dt
                 e2e_n += qb.shape[0]
-        e2e_rate = e2e_n / e2e_t
-        if dist:
-            tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_rate = e2e_n * world / tt.item()
+        e2e_all, (e2e_tmax,) = aggregate(dist, "cuda", e2e_n, [e2e_t])
+        e2e_rate = e2e_all / e2e_tmax
         e2e = {"value": e2e_rate, "unit": "queries/s", "h2d_bytes_per_step": B * w.d * 8,
                "d2h_bytes_per_step": B * w.k * 16 + B * 8,
                "path": "icq_search_host (C ABI, host buffers)"}
