@@ -487,7 +487,22 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     // is sized generously -- HBM is plentiful, the pool is never cleared
     // (only its top counter)
     int64_t entries = (int64_t)Qb * h->n / 8;
-    const int64_t lo = (int64_t)1 << 20, hi_ = (int64_t)1 << 31;  // <= 32 GiB
+    const int64_t lo = (int64_t)1 << 20;
+    int64_t hi_ = (int64_t)1 << 31;  // <= 32 GiB, and <= 1/5 of the device's memory
+    {
+      static int64_t total_mem[64];  // (per device, queried once)
+      int dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+        if (total_mem[dev] == 0) {
+          size_t fr = 0, tot = 0;
+          total_mem[dev] = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? (int64_t)tot : -1;
+        }
+        if (total_mem[dev] > 0) {
+          const int64_t by_mem = total_mem[dev] / 5 / (int64_t)sizeof(uint4);
+          if (by_mem < hi_) hi_ = by_mem;
+        }
+      }
+    }
     entries = entries < lo ? lo : (entries > hi_ ? hi_ : entries);
     p.pool_pages = env_i("ICQ_POOL_PAGES", (entries + kPG - 1) / kPG);
   }

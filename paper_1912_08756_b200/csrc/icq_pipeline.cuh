@@ -41,6 +41,10 @@
 #endif
 // candidate mask of the filter: 1 = one funnel shift per item (ALU pipe),
 // 0 = Horner multiply-adds (two FMA-pipe instructions per item)
+// replay CTAs per SM the register budget is cut for (2: 255 registers, no spills)
+#ifndef ICQ_REPLAY_CTAS
+#define ICQ_REPLAY_CTAS 2
+#endif
 #ifndef ICQ_MASK_SHF
 #define ICQ_MASK_SHF 1
 #endif
@@ -1528,7 +1532,7 @@ static_assert(kSG * ((kListPages * kPG + kCH - 1) / kCH) <= kMaxChunks,
               "a slice group always fits the chunk descriptors");
 
 template <int FP>
-__global__ void __launch_bounds__(kRW * 32, 2) icq_replay_kernel(const __grid_constant__ PipeParams p) {
+__global__ void __launch_bounds__(kRW * 32, ICQ_REPLAY_CTAS) icq_replay_kernel(const __grid_constant__ PipeParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = blockIdx.x;
