@@ -467,8 +467,12 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     // prologue length cap: queries whose stale threshold stays loose are
     // better handed to the filter early (the stop rule ends most queries
     // well before)
+    // (small databases: at most n / 8, the filter and the lists take the rest
+    // -- c1, 100k items: 16k instead of 64k prologue items, 645k -> 790k q/s)
     int64_t pm = h->n / 384;
-    if (pm < ((int64_t)1 << 16)) pm = (int64_t)1 << 16;
+    int64_t floor_ = h->n / 8;
+    floor_ = floor_ < ((int64_t)1 << 14) ? (int64_t)1 << 14 : (floor_ > ((int64_t)1 << 16) ? (int64_t)1 << 16 : floor_);
+    if (pm < floor_) pm = floor_;
     p.pro_max = env_i("ICQ_PRO_MAX", pm);
     // refinement-heavy queries continue in count style (float32 exact
     // pre-filter, ~1 cycle per item): longer, for a tighter T at the hand-over
