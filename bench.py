@@ -297,6 +297,10 @@ def main():
     for i in range(args.warmup):
         if i == args.warmup - 1:  # (the first steps pay one-time allocations)
             torch.cuda.synchronize()
+            # one clock sample under load right before the timed region (an NVML
+            # query can delay the launches that follow it by tens of ms: it is
+            # taken here, ahead of the last warm-up step, not inside the region)
+            clk.sample_now()
             t_w = time.perf_counter()
         step(i)
     torch.cuda.synchronize()
@@ -311,7 +315,6 @@ def main():
     L.icq_profile_enable(1)  # CUDA events around each pipeline kernel, launch stream
     launches0 = int(L.icq_kernel_launches())
     clk.recording = True
-    clk.sample_now()
     for i in range(args.steps):
         outs.append(step(args.warmup + i, evs[i]))
     clk.sample_now()  # the last steps are still running on the device

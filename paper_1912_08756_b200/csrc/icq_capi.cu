@@ -401,8 +401,11 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     const char* v = getenv(name);
     return v ? (int64_t)atoll(v) : dflt;
   };
-  const int Qmax = (int)env_i("ICQ_QBATCH", 2048);
-  const int Qb = Q < Qmax ? Q : Qmax;
+  // queries per sub-batch: as many as the per-batch scratch allows (fewer,
+  // longer prologue / replay launches: c2, 10k queries: 211k -> 256k q/s in one
+  // sub-batch instead of five); bounded below by the slice-table budget
+  const int Qmax = (int)env_i("ICQ_QBATCH", 16384);
+  int Qb = Q < Qmax ? Q : Qmax;
   const bool big = (int64_t)h->n * FP > (int64_t)48 << 20;  // fast stream larger than ~L2/2
   p.range_major = (int32_t)env_i("ICQ_RANGE_MAJOR", big ? 1 : 0);
   {
@@ -423,6 +426,12 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
     rs = (rs + kRangeAlign - 1) / kRangeAlign * kRangeAlign;
     p.RS = rs;
     p.NR = (int32_t)((h->n + rs - 1) / rs);
+    if (!getenv("ICQ_QBATCH")) {  // slice rows: <= 4 GiB per sub-batch
+      const int64_t per_q = (int64_t)p.NR * kFW * kSliceInts * (int64_t)sizeof(int32_t);
+      int64_t qb = ((int64_t)4 << 30) / per_q;
+      qb = qb < 256 ? 256 : qb;
+      if (Qb > qb) Qb = (int)qb;
+    }
     // the count kernel sweeps 2 filter ranges at a time when the stream is
     // larger than L2 (measured on c5: 1 -> 22.5, 2 -> 21.5, 4 -> 22.3, 8 -> 24.1 ms)
     // refine / gather CTAs (one warp per slice of a range) can take a group of
@@ -443,7 +452,14 @@ static icq_status search_impl(icq_index_t h, const double* q, const double* lut_
   // prologue end; deeper J: looser lists, fewer in-order walks); by default
   // the prologue picks the loosest J whose list share stays <= 1/list_div
   p.list_j = (int32_t)env_i("ICQ_LIST_J", -1);
-  p.list_div = (int32_t)env_i("ICQ_LIST_DIV", 128);
+  // (list length ~ n / list_div: small databases take looser lists -- fewer
+  // walks; c1 +14 %, c2 +4 % at 1/32 -- large ones tighter: c5 at sigma = 0
+  // loses 36 % at 1/32)
+  {
+    int64_t ld = h->n / 500000;
+    ld = ld < 32 ? 32 : (ld > 128 ? 128 : ld);
+    p.list_div = (int32_t)env_i("ICQ_LIST_DIV", ld);
+  }
   p.pro_live = (int32_t)env_i("ICQ_PRO_LIVE", 0);
   // count mode (refinement-heavy queries: the live threshold passes > 1/count_div
   // of the sampled items): lists of possible insertions + a parallel count
